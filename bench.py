@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py — scheduling decisions/s of the B200 Orloj batch-scoring path.
+
+Default (N = 1): workload C3: 65,536 queues x 256 requests with
+per-request 256-bin histograms (16.8 M rows, 17.2 GB log2-CDF store in HBM),
+kmax = 256.  One step = one orloj_pick_batch over all queues (rows a1-a6 of
+SURVEY §8(a)); inputs (17.4 GB per step) are larger than L2, so no flush is
+needed between steps.  The store is built once, off the timed region (a0; the
+paper's profiler is off the critical path).
+
+Also measured in the same run (sub-objects of the one JSON line):
+  e2e          the same pick through orloj_pick_batch_host, with the queue
+               arrays copied from pinned host memory and results copied back
+               inside the timed region;
+  replay       the C5 trace-replay sweep (rows a7-a8): 4 families x 8 SLO
+               buckets x 256 seeds x 100k arrivals, scenarios sharded
+               round-robin over ranks, one NCCL all-reduce of the counters;
+  roofline     HBM roofline of the dominant kernel (the pick kernel);
+  cpu_baseline the fp64 oracle on a bounded C3 sample on the host cores.
+
+Multi-GPU (torchrun): every rank picks its own C3 instance (weak scaling, no
+collective on the score path); value = all ranks' decisions / max-over-ranks
+time.  --impl reference times the oracle (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scheduling decisions/sec and candidate batches/sec @1/2/4/8 B200; HBM GB/s % peak"
+WORKLOAD = ("C3: 65,536 queues x 256 requests x 256-bin per-request histograms (BART-CNN-like, "
+            "mean 774.66 / P99 1101.99 ms), kmax = 256, 16.8 M permuted 1 KB rows (17.2 GB store)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="orloj", choices=["orloj", "reference"])
+    ap.add_argument("--queues", type=int, default=65536)
+    ap.add_argument("--kmax", type=int, default=256)
+    ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--replay-seeds", type=int, default=256, help="seeds per (family, bucket)")
+    ap.add_argument("--replay-arrivals", type=int, default=100_000)
+    ap.add_argument("--replay-reps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profiling mode: only the timed pick loop")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------
+# clocks sampled during the timed region (NVML)
+# ----------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"error": getattr(self, "err", "nvml unavailable")}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, STREAM-style copy)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the pick kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_c3_pick_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+# ----------------------------------------------------------------------------
+# oracle timing (cpu_baseline leg and the --impl reference arm)
+# ----------------------------------------------------------------------------
+
+def oracle_c3_sample(cfg, nq: int, start: int = 0):
+    import gen
+    sub = cfg.queues.subset(np.arange(start, start + nq))
+    rows = gen.rows_host(cfg.row_seed, sub.dist.astype(np.uint64), cfg.fam.counts)
+    local = gen.Queues(sub.offsets, sub.arrival, sub.deadline, np.arange(len(sub.dist), dtype=np.int32), sub.now)
+    return rows, local
+
+
+def time_oracle_c3(cfg, seconds: float, chunk: int = 64):
+    """Run the oracle on consecutive chunks of C3 queues until `seconds` of work."""
+    import oracle
+    done, t_or, start = 0, 0.0, 0
+    while t_or < seconds and start + chunk <= cfg.queues.Q:
+        rows, local = oracle_c3_sample(cfg, chunk, start)
+        t0 = time.perf_counter()
+        F = oracle.cdf(rows)
+        oracle.score(F, cfg.profile.a, cfg.profile.w, local.offsets, local.deadline, local.dist, local.now)
+        t_or += time.perf_counter() - t0
+        done += chunk
+        start += chunk
+    return done, t_or, oracle.max_threads()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import gen
+    cfg = gen.config3(Q=args.queues, kmax=args.kmax)
+    per_step = 128
+    import oracle
+    secs = []
+    for s in range(args.warmup + args.steps):
+        rows, local = oracle_c3_sample(cfg, per_step, (s * per_step) % (cfg.queues.Q - per_step))
+        t0 = time.perf_counter()
+        oracle.score(oracle.cdf(rows), cfg.profile.a, cfg.profile.w, local.offsets, local.deadline, local.dist,
+                     local.now)
+        if s >= args.warmup:
+            secs.append(time.perf_counter() - t0)
+    t = float(np.sum(secs))
+    val = per_step * len(secs) / t
+    cores = oracle.max_threads()
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "decisions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / len(secs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "step": f"{per_step} C3 queues on the host (bounded sample)"},
+        "cpu_baseline": {"value": val, "unit": "decisions/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} consecutive C3 queues per step, fp64 oracle, all host threads"},
+        "e2e": {"value": val, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    # ---------------- C3 pick: setup (untimed) ----------------
+    cfg = gen.config3(Q=args.queues, kmax=args.kmax, instance=rank)
+    store = wl.c3_store(cfg, dev)
+    prof = wl.profile(cfg.profile)
+    qn = cfg.queues
+    qs = wl.device_queues(qn, dev, with_arrival=False)
+    Q = qn.Q
+    K = np.minimum(np.diff(qn.offsets), cfg.kmax)
+    cands = int(K.sum())
+    B = cfg.fam.B
+    algo_bytes = (cands * B * 4                      # log2-CDF rows gathered
+                  + int(K.sum()) * (8 + 4)           # deadline + dist id per candidate member
+                  + (Q + 1) * 8 + Q * 8              # offsets, now
+                  + Q * (4 + 4))                     # best_k, best_E
+    bk = torch.empty(Q, dtype=torch.int32, device=dev)
+    bE = torch.empty(Q, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        orj.pick_batch(store, prof, qs, bk, bE, stream)
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            orj.pick_batch(store, prof, qs, bk, bE, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_total)
+    ms_step = ms_total / args.steps
+    value = world * Q / (ms_step / 1e3)
+    cand_s = world * cands / (ms_step / 1e3)
+    achieved = algo_bytes / (ms_step / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    traffic = ncu_traffic()
+    result = {
+        "metric": METRIC, "value": value, "unit": "decisions/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY §8(d) recipe, DESIGN.md §4)",
+        "config": {"workload": WORKLOAD, "queues_per_gpu": Q, "requests_per_queue": int(np.diff(qn.offsets)[0]),
+                   "bins": B, "kmax": cfg.kmax, "global_queues": world * Q,
+                   "l2": "inputs larger than L2 (17.4 GB read per step); no flush",
+                   "parallelism": f"queues sharded, {world} independent C3 instances, no collective"},
+        "candidates_per_s": cand_s,
+        "hbm_gbs_algorithmic": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "score_kernel<8,8,PICK,STREAM> (orloj_pick_batch)",
+                     "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    if args.ncu:
+        if rank == 0:
+            print(json.dumps(result), flush=True)
+        return
+
+    # ---------------- e2e: host buffers through orloj_pick_batch_host ----------------
+    if not args.no_e2e:
+        pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()  # noqa: E731
+        h_off, h_dl = pin(qn.offsets, np.int64), pin(qn.deadline, np.int64)
+        h_dist, h_now = pin(qn.dist, np.int32), pin(qn.now, np.int64)
+        hp = orj.HostPicker(store, prof, Q, qn.N, dev)
+        for _ in range(max(1, args.warmup)):
+            hp.pick(h_off, h_dl, h_dist, h_now, stream)
+        torch.cuda.synchronize()
+        barrier()
+        e_steps = max(5, args.steps // 5)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e_steps):
+            hp.pick(h_off, h_dl, h_dist, h_now, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1)) / e_steps
+        assert (hp.best_k.numpy() == bk.cpu().numpy()).all()
+        result["e2e"] = {"value": world * Q / (e_ms / 1e3), "unit": "decisions/s",
+                         "h2d_bytes_per_step": hp.h2d_bytes(), "d2h_bytes_per_step": hp.d2h_bytes(),
+                         "ms_per_step": e_ms, "steps": e_steps,
+                         "path": "orloj_pick_batch_host: pinned host queues -> H2D -> kernel -> D2H, one stream"}
+        del hp
+
+    # ---------------- cpu baseline (rank 0, N = 1 only) ----------------
+    if world == 1 and not args.no_cpu_baseline:
+        n, secs, cores = time_oracle_c3(cfg, args.cpu_seconds)
+        result["cpu_baseline"] = {"value": n / secs, "unit": "decisions/s", "cores": cores, "kind": "oracle",
+                                  "sample": f"first {n} C3 queues (256 x 256 bins, kmax 256), fp64 oracle, "
+                                            f"{secs:.1f} s on {cores} host threads"}
+    else:
+        result["cpu_baseline"] = None
+
+    del store, qs
+    torch.cuda.empty_cache()
+
+    # ---------------- replay sweep (C5) ----------------
+    if not args.no_replay:
+        result["replay"] = run_replay(args, rank, world, dev, barrier, max_over_ranks)
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_replay(args, rank, world, dev, barrier, max_over_ranks):
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+    from paper_2209_00159_b200 import parallel
+
+    fams = []
+    for name in gen.C5_FAMILIES:
+        nb = len(gen.BUCKET_SLO_MULTS)
+        u = np.arange(nb * args.replay_seeds)
+        mine = parallel.shard_round_robin(u // nb, rank, world)    # seed groups round-robin
+        fams.append(wl.C5Family(name, local_ids=mine, n_arr=args.replay_arrivals,
+                                seeds_per_bucket=args.replay_seeds, device=dev))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(dev) for _ in fams]
+    main = torch.cuda.current_stream()
+    nb = len(gen.BUCKET_SLO_MULTS)
+    tables = [torch.zeros((nb, 7), dtype=torch.int64, device=dev) for _ in fams]
+
+    def once():
+        for t_ in tables:
+            t_.zero_()
+        start = torch.cuda.Event()
+        start.record(main)
+        for f, s, t_ in zip(fams, streams, tables):
+            s.wait_event(start)
+            orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, stream=s)
+        for s in streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            main.wait_event(ev)
+
+    once()  # warm-up
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(main)
+        for _ in range(args.replay_reps):
+            once()
+        e1.record(main)
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.replay_reps
+    per_family = {}
+    total = torch.zeros((nb, 7), dtype=torch.int64, device=dev)
+    for f, t_ in zip(fams, tables):
+        parallel.allreduce_counters(t_)          # one NCCL all-reduce per family table
+        per_family[f.tf.fam.name] = t_.cpu().numpy()
+        total += t_
+    tot = total.cpu().numpy()
+    decisions = int(tot[:, 4].sum())
+    arrivals = int(tot[:, 0].sum())
+    assert (tot[:, 1] + tot[:, 2] + tot[:, 3] == tot[:, 0]).all()
+    fr = {name: [round(float(x), 4) for x in (c[:, 1] / np.maximum(c[:, 0], 1))] for name, c in per_family.items()}
+    util = {name: round(float(c[:, 5].sum() / max(c[:, 6].sum(), 1)), 4) for name, c in per_family.items()}
+    return {"workload": f"C5: 4 families x 8 SLO buckets x {args.replay_seeds} seeds x {args.replay_arrivals} "
+                        f"arrivals (kmax 32, B 64), scenarios round-robin over {world} ranks",
+            "value": decisions / (ms / 1e3), "unit": "decisions/s", "arrivals_per_s": arrivals / (ms / 1e3),
+            "ms_per_sweep": ms, "decisions": decisions, "arrivals": arrivals, "scaling": "strong",
+            "finish_rate_by_bucket": fr, "slo_multipliers": list(gen.BUCKET_SLO_MULTS), "utilisation": util,
+            "gpu_launches_per_sweep": len(fams), "clocks": clk.summary(),
+            "collective": "torch.distributed.all_reduce(int64 [8x7]) per family (NCCL) after the timed region"}
+
+
+if __name__ == "__main__":
+    main()

@@ -265,8 +265,11 @@ def snapshot_queues(seed: int, lengths, slo_base_ticks: int, dist_ids=None, D: i
     qid = np.repeat(np.arange(Q), lengths)
     ages = np.floor(u * slo[qid]).astype(np.int64)
     # sort ages descending within each queue
-    order = np.lexsort((-ages, qid))
-    ages = ages[order]
+    if Q and (lengths == lengths[0]).all():
+        ages = -np.sort(-ages.reshape(Q, -1), axis=1).reshape(-1)
+    else:
+        order = np.lexsort((-ages, qid))
+        ages = ages[order]
     arrival = now[qid] - ages
     deadline = arrival + slo[qid]
     if dist_ids is None:
@@ -313,17 +316,18 @@ def config2(Q: int = 1024, n: int = 64, kmax: int = 32) -> ScoreConfig:
     return ScoreConfig("C2", fam, prof, q)
 
 
-def config3(Q: int = 65536, n: int = 256, kmax: int = 256, T: int = 4096) -> ScoreConfig:
+def config3(Q: int = 65536, n: int = 256, kmax: int = 256, T: int = 4096, instance: int = 0) -> ScoreConfig:
     """Per-request rows: row ids are a seeded random permutation of [0, Q*n), so
-    every candidate is a true 1 KB gather."""
+    every candidate is a true 1 KB gather.  `instance` selects an
+    independent draw of rows and queues (one per rank under weak scaling)."""
     seed = SEED_BASE + 3
     fam = bart_templates(seed, T=T)
     prof = eq3_half(fam, kmax)
-    rng = np.random.default_rng(seed + 1000)
+    rng = np.random.default_rng(seed + 1000 + 7919 * instance)
     n_rows = Q * n
     perm = rng.permutation(n_rows).astype(np.int32)
-    q = snapshot_queues(seed, np.full(Q, n), fam.p99_ticks(), dist_ids=perm)
-    return ScoreConfig("C3", fam, prof, q, rows="c3", n_rows=n_rows, row_seed=seed)
+    q = snapshot_queues(seed + 7919 * instance, np.full(Q, n), fam.p99_ticks(), dist_ids=perm)
+    return ScoreConfig("C3", fam, prof, q, rows="c3", n_rows=n_rows, row_seed=seed + 7919 * instance)
 
 
 def config4(Q: int = 1 << 20, n: int = 32, kmax: int = 32, near: bool = False) -> ScoreConfig:

@@ -1,0 +1,215 @@
+/*
+ * orloj.h — C ABI of the B200-native Orloj batch-scoring library (liborloj.so).
+ *
+ * Orloj (arXiv 2209.00159) schedules batches of requests whose execution time
+ * is a random variable known only through an empirical histogram per
+ * application (PAPER.md:241-255 problem statement, :377-383 per-application
+ * tracking).  This library evaluates, on the GPU and for very many independent
+ * queues at once, the paper's batch execution-time model on every candidate
+ * batch = every deadline-ordered prefix of a queue:
+ *
+ *   batch time     L_{B_k} = a_k + w_k * max_{j<=k} X_j          Eq. 3-4 (:479-491),
+ *                                                                 Eq. 9 CDF form (:537-541)
+ *   CDF of the max G_k(tau_i) = prod_{j<=k} F_{d_j}(tau_i)        Eq. 6 (:503-507), Eq. 8 (:512-535)
+ *   finish prob.   P_r(k) = Pr(t + L_{B_k} <= D_r) = G_k(tau_{i*}) step SLO cost (:411-419)
+ *                  i*(r,k) = clamp(floor((D_r - t - a_k) / w_k), 0, B)
+ *   objective      E_k = sum_{r<=k} P_r(k), k* = smallest argmax  (:419-421)
+ *   optional       E[L_{B_k}] = a_k + w_k * E[max bin]             Eq. 5 (:493-502)
+ *
+ * and replays request traces through the resulting decision rule (admit, drop
+ * hopeless, pick, dispatch non-preemptively).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns an orloj_status; 0 = OK.  On failure, orloj_last_error()
+ *    returns a thread-local message describing the last error on this thread.
+ *  - Time is int64 "ticks" (1 tick = 1 us in the shipped workloads); only
+ *    differences (D_r - t) enter the arithmetic, so absolute timestamps may be
+ *    large (PAPER.md:612-623 overflow discussion).
+ *  - Bins: a store has B bins, bin i (1..B) standing for tau_i = i * Delta, the
+ *    upper bin edge (mass "discrete at upper edges", reading A1).
+ *  - Buffers marked "device" are CUDA device pointers (e.g. torch CUDA tensor
+ *    storage); "host" are host pointers ("pinned host" where the call copies
+ *    asynchronously).  The caller owns every buffer.  The hot calls
+ *    (score / pick / replay) never allocate, keep no global mutable state,
+ *    and only enqueue work on `stream` (a cudaStream_t passed as void*; NULL =
+ *    legacy default stream).  Calls on distinct streams are independent.
+ *  - O(1) argument errors are detected and returned synchronously, before any
+ *    work is enqueued.  Faults inside kernels surface as ORLOJ_ERR_CUDA at the
+ *    next call or stream synchronisation (CUDA convention).  Expensive O(N)
+ *    input checks live in orloj_validate_* (synchronous, not hot).
+ */
+#ifndef ORLOJ_H
+#define ORLOJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORLOJ_ABI_VERSION 1
+#define ORLOJ_MAX_KMAX 256        /* candidate batch sizes per queue (score / pick) */
+#define ORLOJ_MAX_BINS 256        /* bins per histogram (score / pick) */
+#define ORLOJ_REPLAY_MAX_KMAX 32  /* window size in replay */
+#define ORLOJ_REPLAY_MAX_BINS 128 /* bins per histogram in replay */
+
+typedef enum {
+  ORLOJ_OK = 0,
+  ORLOJ_ERR_INVALID_ARGUMENT = 1, /* bad pointer / size / profile (non-monotone, w_k < 1, ...) */
+  ORLOJ_ERR_COLD_START = 2,       /* a histogram has total count 0 */
+  ORLOJ_ERR_UNSORTED = 3,         /* queue / trace order violated (validation only) */
+  ORLOJ_ERR_CAPACITY = 4,         /* beyond built limits (kmax, B, 2^31-tick horizon, store size) */
+  ORLOJ_ERR_CUDA = 5,             /* CUDA runtime / launch error */
+  ORLOJ_ERR_OOM = 6               /* scratch allocation failed (validation / store build only) */
+} orloj_status;
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *orloj_last_error(void);
+
+/* ORLOJ_ABI_VERSION of the loaded library. */
+int32_t orloj_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Histogram / CDF store.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t num_dists;     /* D >= 1 */
+  int32_t num_bins;      /* B: multiple of 4, 4 <= B <= ORLOJ_MAX_BINS */
+  int64_t bin_ticks;     /* Delta > 0 (informational: kernels work in bin units via the profile) */
+  const float *log2_cdf; /* device [D][B] row-major, 16-byte aligned:
+                            element [d][i-1] = log2 F_d(tau_i) rounded to fp32 (RN);
+                            -inf where F = 0; [d][B-1] == 0.0f exactly (F_d(tau_B) = 1). */
+} orloj_store;
+
+/* Build log2_cdf rows from integer counts: F_d(tau_i) = cum_i / total_d in fp64,
+ * log2 in fp64, rounded once to fp32.  counts: device uint32 [D][B]; out: device
+ * float [D][B] (caller-allocated, 16-byte aligned).  Rows may be built in chunks
+ * by offsetting both pointers.  Synchronises `stream` (off the hot path: the
+ * paper's profiler runs off the critical path) and may allocate
+ * 4 bytes of scratch.  Errors: INVALID_ARGUMENT (sizes / alignment),
+ * COLD_START (some row has total 0; rows already written are left as written),
+ * CUDA, OOM. */
+orloj_status orloj_store_build(const uint32_t *counts, int32_t num_dists, int32_t num_bins,
+                               float *log2_cdf_out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Latency profile: Eq. 3 generalised to a monotone integer table (A3).
+ * A batch of k whose slowest member lies in bin m runs a_k + w_k * m ticks.
+ * Eq. 3 (l_B = c0 + c1 k l) is the preset a_k = round(c0), w_k = round(c1 k Delta).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t kmax;                 /* 1 <= kmax <= ORLOJ_MAX_KMAX (replay: <= ORLOJ_REPLAY_MAX_KMAX) */
+  const int64_t *offset_ticks;  /* host [kmax]: a_k >= 0, non-decreasing in k */
+  const int64_t *ticks_per_bin; /* host [kmax]: w_k >= 1, non-decreasing in k */
+} orloj_latency_profile;
+/* The table is copied into kernel parameters at each call (host pointers need
+ * only be valid during the call).  Monotonicity (A14) is required
+ * (INVALID_ARGUMENT otherwise): it makes P_r(k+1) <= P_r(k) hold bit-exactly.
+ * Horizon: a_kmax + w_kmax * B must be <= 2^31 - 1 ticks (CAPACITY otherwise),
+ * so bin lookups run in exact 32-bit integer arithmetic. */
+
+/* ---------------------------------------------------------------------------
+ * Queues (release time, deadline = release + SLO, and an
+ * execution-time distribution through the application id, :377-383).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t num_queues;            /* Q >= 0 */
+  const int64_t *queue_offsets;  /* device [Q+1], CSR: queue q = members [off[q], off[q+1]) */
+  const int64_t *arrival_ticks;  /* device [N] release times, or NULL; read only by validation (tie order) */
+  const int64_t *deadline_ticks; /* device [N]; per queue ordered by (deadline, arrival, index) (A9) */
+  const int32_t *dist_id;        /* device [N], 0 <= dist_id < store.num_dists */
+  const int64_t *now_ticks;      /* device [Q]: decision time t of each queue */
+} orloj_queues;
+/* score / pick take each queue as given: candidates are its first
+ * K_q = min(n_q, kmax) members; hopeless members simply score P = 0. */
+
+/* Score every candidate batch of every queue.
+ *   expected_finish      device float [Q][kmax]: E_k at [q][k-1]; entries k > K_q are 0.
+ *   finish_prob          device float [Q][kmax(kmax+1)/2] or NULL: P_r(k) at
+ *                        [q][k(k-1)/2 + r], r = 0..k-1 (0-based member), k = 1..kmax;
+ *                        entries with k > K_q are left untouched.
+ *   expected_batch_ticks device float [Q][kmax] or NULL: E[L_{B_k}] (Eq. 5); 0 for k > K_q.
+ * Accuracy: |P - P_exact| <= 1e-5, |E_k - E_exact| <= 1e-5 k.
+ * Errors: INVALID_ARGUMENT, CAPACITY (B > 256, kmax > 256, horizon), CUDA. */
+orloj_status orloj_score_batches(const orloj_store *store, const orloj_latency_profile *profile,
+                                 const orloj_queues *queues, float *expected_finish,
+                                 float *finish_prob, float *expected_batch_ticks, void *stream);
+
+/* Pick the batch size of every queue: k* = argmax_k E_k,
+ * ties -> smallest k (A10).  best_k: device int32 [Q] (0 iff the queue is
+ * empty); best_expected: device float [Q] (E_{k*}; 0 for empty queues).
+ * Same kernel as score_batches with a fused warp-reduction epilogue. */
+orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_profile *profile,
+                              const orloj_queues *queues, int32_t *best_k, float *best_expected,
+                              void *stream);
+
+/* End-to-end variant of orloj_pick_batch for queues that live in (pinned) host
+ * memory: enqueues H2D copies of the queue arrays into `workspace`, the pick
+ * kernel and D2H copies of the results, all on `stream`; the caller
+ * synchronises.  Host arrays must stay valid until the stream reaches the
+ * copies.  workspace: device, >= orloj_pick_batch_host_workspace(Q, N) bytes,
+ * 256-byte aligned. */
+size_t orloj_pick_batch_host_workspace(int64_t num_queues, int64_t num_members);
+orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency_profile *profile,
+                                   int64_t num_queues, const int64_t *queue_offsets_host,
+                                   const int64_t *deadline_ticks_host, const int32_t *dist_id_host,
+                                   const int64_t *now_ticks_host, int32_t *best_k_host,
+                                   float *best_expected_host, void *workspace,
+                                   size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Trace replay (readings A9, A11, A15-A17).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t num_scenarios;           /* S >= 0 */
+  const int64_t *arrival_offsets;  /* device [S+1], CSR over arrivals */
+  const int64_t *arrival_ticks;    /* device [N], non-decreasing within a scenario */
+  const int32_t *dist_id;          /* device [N] */
+  const int16_t *true_bin;         /* device [N], 1..B: hidden execution time, used only at dispatch */
+  const int64_t *slo_ticks;        /* device [S] >= 0: deadline = arrival + slo (constant per scenario) */
+  const int32_t *bucket;           /* device [S], 0 <= bucket < num_buckets */
+  int32_t num_buckets;             /* >= 1 */
+} orloj_trace;
+
+typedef struct {
+  int64_t total;      /* arrivals */
+  int64_t finished;   /* completed with end <= deadline (A11) */
+  int64_t dropped;    /* dropped as hopeless: P_r(1) = 0 (A16) */
+  int64_t late;       /* dispatched, completed after the deadline (A17) */
+  int64_t batches;    /* decisions = dispatched batches */
+  int64_t busy_ticks; /* sum of batch durations */
+  int64_t span_ticks; /* end of last batch - first arrival */
+} orloj_counters;
+
+/* Replay every scenario on a single non-preemptive worker.  Per scenario, in
+ * this order, until every arrival is handled: (1) if nothing is queued, jump to
+ * the next arrival (work-conserving, A15); (2) scan the live queue (window
+ * remainder first, then arrivals <= t) from the head, dropping each hopeless
+ * request and collecting the others into a window of <= kmax (A16); (3) pick
+ * k* on the window exactly as orloj_pick_batch; (4) dispatch the first k*:
+ * dur = a_k* + w_k* * max true_bin; finished / late by the deadline; (5) t += dur.
+ * per_bucket: device [num_buckets]; counters are ADDED (atomics), so zero them
+ * first.  decision_log: device int32 [N + S] or NULL; decision d of scenario s
+ * is written at [arrival_offsets[s] + s + d], followed by a 0.
+ * Limits: kmax <= 32, B <= 128, D*B*4 <= 64 KiB (CAPACITY otherwise). */
+orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
+                                const orloj_trace *trace, orloj_counters *per_bucket,
+                                int32_t *decision_log, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Validation (synchronous, O(N), not hot; may allocate a few bytes of scratch).
+ * ------------------------------------------------------------------------- */
+/* rows non-decreasing, <= 0, no NaN, [d][B-1] == 0.0f.  INVALID_ARGUMENT otherwise. */
+orloj_status orloj_validate_store(const orloj_store *store, void *stream);
+/* offsets monotone from 0; dist ids in range (INVALID_ARGUMENT); per-queue
+ * (deadline, arrival, index) order (UNSORTED; arrival used when non-NULL). */
+orloj_status orloj_validate_queues(const orloj_store *store, const orloj_queues *queues, void *stream);
+/* offsets monotone from 0, ids / bins / buckets in range, slo >= 0 (INVALID_ARGUMENT);
+ * arrivals non-decreasing per scenario (UNSORTED). */
+orloj_status orloj_validate_trace(const orloj_store *store, const orloj_trace *trace, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORLOJ_H */

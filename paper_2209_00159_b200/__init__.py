@@ -1,0 +1,298 @@
+"""paper_2209_00159_b200 — B200-native distribution-aware batch scoring (Orloj).
+
+Thin Python binding over the C ABI in ``include/orloj.h`` (liborloj.so, CUDA
+sm_100a).  This module only marshals arguments: every step of the hot path
+(store build, candidate gather, log2-domain prefix products, bin lookup,
+finish probabilities, expected finish counts, argmax, trace replay) runs in the
+library's kernels.  PyTorch supplies device memory, streams and process
+groups.  There is no CPU fallback: a missing library raises ``OrlojError``.
+
+Names follow the paper (PAPER.md :241-255, Eq. 3-9 :477-543) and SURVEY.md §0.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import OrlojError, build  # noqa: F401
+from .parallel import allreduce_counters, shard_blocks, shard_round_robin  # noqa: F401
+
+COUNTER_FIELDS = ("total", "finished", "dropped", "late", "batches", "busy_ticks", "span_ticks")
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise OrlojError(1, f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise OrlojError(1, f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise OrlojError(1, f"{name} must be contiguous")
+    return t
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+# ----------------------------------------------------------------------------
+# store
+# ----------------------------------------------------------------------------
+
+class HistogramStore:
+    """HBM-resident log2-CDF rows, one per distribution (application or request).
+
+    ``log2_cdf[d, i-1] = log2 F_d(tau_i)`` in fp32; built from integer counts by
+    ``orloj_store_build`` (PAPER.md:377-394 per-application histograms)."""
+
+    def __init__(self, log2_cdf: torch.Tensor, bin_ticks: int):
+        self.log2_cdf = _dev(log2_cdf, torch.float32, "log2_cdf")
+        if log2_cdf.dim() != 2:
+            raise OrlojError(1, "log2_cdf must be [D, B]")
+        self.bin_ticks = int(bin_ticks)
+        self._c = _abi.Store(log2_cdf.shape[0], log2_cdf.shape[1], self.bin_ticks, log2_cdf.data_ptr())
+
+    @property
+    def num_dists(self):
+        return self.log2_cdf.shape[0]
+
+    @property
+    def num_bins(self):
+        return self.log2_cdf.shape[1]
+
+    @classmethod
+    def empty(cls, num_dists: int, num_bins: int, bin_ticks: int, device="cuda") -> "HistogramStore":
+        return cls(torch.empty((num_dists, num_bins), dtype=torch.float32, device=device), bin_ticks)
+
+    def build_rows(self, counts: torch.Tensor, row0: int = 0, stream=None):
+        """Fill rows [row0, row0 + len(counts)) from integer counts (device
+        int32/uint32 [n, B], reinterpreted as uint32).  Synchronises the stream."""
+        if counts.dtype == torch.uint32:
+            counts = counts.view(torch.int32)
+        counts = _dev(counts, torch.int32, "counts")
+        n, B = counts.shape
+        if B != self.num_bins or row0 < 0 or row0 + n > self.num_dists:
+            raise OrlojError(1, "counts shape / row range does not fit the store")
+        out = self.log2_cdf[row0:row0 + n]
+        _abi.check(_abi.lib().orloj_store_build(counts.data_ptr(), n, B, out.data_ptr(), _stream_ptr(stream)))
+        return self
+
+    @classmethod
+    def from_counts(cls, counts, bin_ticks: int, device="cuda", stream=None) -> "HistogramStore":
+        if isinstance(counts, np.ndarray):
+            counts = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.uint32).view(np.int32))
+        counts = counts.to(device)
+        st = cls.empty(counts.shape[0], counts.shape[1], bin_ticks, device)
+        return st.build_rows(counts, 0, stream)
+
+    def validate(self, stream=None):
+        _abi.check(_abi.lib().orloj_validate_store(ctypes.byref(self._c), _stream_ptr(stream)))
+
+    def c(self):
+        return ctypes.byref(self._c)
+
+
+# ----------------------------------------------------------------------------
+# latency profile (Eq. 3 generalised, A3)
+# ----------------------------------------------------------------------------
+
+class LatencyProfile:
+    """a_k (offset ticks) and w_k (ticks per bin), k = 1..kmax, non-decreasing."""
+
+    def __init__(self, offset_ticks, ticks_per_bin):
+        self.a = np.ascontiguousarray(offset_ticks, dtype=np.int64)
+        self.w = np.ascontiguousarray(ticks_per_bin, dtype=np.int64)
+        if self.a.shape != self.w.shape or self.a.ndim != 1:
+            raise OrlojError(1, "offset_ticks / ticks_per_bin must be 1-D of equal length")
+        self._c = _abi.LatencyProfile(len(self.a), self.a.ctypes.data, self.w.ctypes.data)
+
+    @classmethod
+    def eq3(cls, c0_ticks: float, c1: float, bin_ticks: int, kmax: int) -> "LatencyProfile":
+        """Eq. 3 on the bin grid: a_k = round(c0), w_k = round(c1 k Delta)."""
+        k = np.arange(1, kmax + 1)
+        return cls(np.full(kmax, int(round(c0_ticks))), np.array([int(round(c1 * kk * bin_ticks)) for kk in k]))
+
+    @property
+    def kmax(self):
+        return len(self.a)
+
+    def c(self):
+        return ctypes.byref(self._c)
+
+
+# ----------------------------------------------------------------------------
+# queues + score / pick
+# ----------------------------------------------------------------------------
+
+@dataclass
+class Queues:
+    """CSR queues on the device, members in (deadline, arrival, index) order."""
+    offsets: torch.Tensor    # int64 [Q+1]
+    deadline: torch.Tensor   # int64 [N]
+    dist: torch.Tensor       # int32 [N]
+    now: torch.Tensor        # int64 [Q]
+    arrival: Optional[torch.Tensor] = None  # int64 [N], validation only
+
+    def __post_init__(self):
+        _dev(self.offsets, torch.int64, "offsets")
+        _dev(self.deadline, torch.int64, "deadline")
+        _dev(self.dist, torch.int32, "dist")
+        _dev(self.now, torch.int64, "now")
+        if self.arrival is not None:
+            _dev(self.arrival, torch.int64, "arrival")
+        self._c = _abi.QueuesC(self.now.numel(), self.offsets.data_ptr(), _ptr(self.arrival),
+                               self.deadline.data_ptr(), self.dist.data_ptr(), self.now.data_ptr())
+
+    @property
+    def num_queues(self):
+        return self.now.numel()
+
+    @classmethod
+    def from_numpy(cls, offsets, deadline, dist, now, arrival=None, device="cuda") -> "Queues":
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)  # noqa: E731
+        return cls(t(offsets, np.int64), t(deadline, np.int64), t(dist, np.int32), t(now, np.int64),
+                   None if arrival is None else t(arrival, np.int64))
+
+    def validate(self, store: HistogramStore, stream=None):
+        _abi.check(_abi.lib().orloj_validate_queues(store.c(), ctypes.byref(self._c), _stream_ptr(stream)))
+
+    def c(self):
+        return ctypes.byref(self._c)
+
+
+def score_batches(store: HistogramStore, profile: LatencyProfile, queues: Queues, want_P: bool = False,
+                  want_EL: bool = False, stream=None, out: Optional[dict] = None) -> dict:
+    """E_k for every candidate prefix (+ optional P_r(k), E[L_{B_k}]).  Async on `stream`."""
+    Q, kmax = queues.num_queues, profile.kmax
+    dev = queues.now.device
+    out = out or {}
+    E = out.get("E")
+    if E is None:
+        E = torch.empty((Q, kmax), dtype=torch.float32, device=dev)
+    P = out.get("P") if want_P else None
+    if want_P and P is None:
+        P = torch.zeros((Q, kmax * (kmax + 1) // 2), dtype=torch.float32, device=dev)
+    EL = out.get("EL") if want_EL else None
+    if want_EL and EL is None:
+        EL = torch.empty((Q, kmax), dtype=torch.float32, device=dev)
+    _abi.check(_abi.lib().orloj_score_batches(store.c(), profile.c(), queues.c(), E.data_ptr(), _ptr(P),
+                                              _ptr(EL), _stream_ptr(stream)))
+    return {"E": E, "P": P, "EL": EL}
+
+
+def pick_batch(store: HistogramStore, profile: LatencyProfile, queues: Queues, best_k=None, best_E=None,
+               stream=None):
+    """k* = smallest argmax_k E_k per queue (0 for empty queues) and E_{k*}.  Async."""
+    Q = queues.num_queues
+    dev = queues.now.device
+    if best_k is None:
+        best_k = torch.empty(Q, dtype=torch.int32, device=dev)
+    if best_E is None:
+        best_E = torch.empty(Q, dtype=torch.float32, device=dev)
+    _abi.check(_abi.lib().orloj_pick_batch(store.c(), profile.c(), queues.c(), best_k.data_ptr(),
+                                           best_E.data_ptr(), _stream_ptr(stream)))
+    return best_k, best_E
+
+
+class HostPicker:
+    """End-to-end pick for queues in pinned host memory (orloj_pick_batch_host):
+    H2D copies, kernel and D2H copies enqueued by the library on one stream."""
+
+    def __init__(self, store: HistogramStore, profile: LatencyProfile, num_queues: int, num_members: int,
+                 device="cuda"):
+        self.store, self.profile = store, profile
+        self.Q, self.N = int(num_queues), int(num_members)
+        nbytes = _abi.lib().orloj_pick_batch_host_workspace(self.Q, self.N)
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        base = self.workspace.data_ptr()
+        self._ws = (base + 255) & ~255
+        self._ws_bytes = nbytes
+        self.best_k = torch.empty(self.Q, dtype=torch.int32).pin_memory()
+        self.best_E = torch.empty(self.Q, dtype=torch.float32).pin_memory()
+
+    def h2d_bytes(self):
+        return (self.Q + 1) * 8 + self.N * 8 + self.N * 4 + self.Q * 8
+
+    def d2h_bytes(self):
+        return self.Q * 8
+
+    def pick(self, offsets: torch.Tensor, deadline: torch.Tensor, dist: torch.Tensor, now: torch.Tensor,
+             stream=None):
+        for t, dt, n in ((offsets, torch.int64, "offsets"), (deadline, torch.int64, "deadline"),
+                         (dist, torch.int32, "dist"), (now, torch.int64, "now")):
+            if t.is_cuda or t.dtype != dt or not t.is_contiguous():
+                raise OrlojError(1, f"{n} must be a contiguous host {dt} tensor (pinned for async copies)")
+        _abi.check(_abi.lib().orloj_pick_batch_host(
+            self.store.c(), self.profile.c(), self.Q, offsets.data_ptr(), deadline.data_ptr(), dist.data_ptr(),
+            now.data_ptr(), self.best_k.data_ptr(), self.best_E.data_ptr(), self._ws, self._ws_bytes,
+            _stream_ptr(stream)))
+        return self.best_k, self.best_E
+
+
+# ----------------------------------------------------------------------------
+# trace replay
+# ----------------------------------------------------------------------------
+
+@dataclass
+class Trace:
+    """Arrival trace of many independent scenarios (CSR), constant SLO each."""
+    offsets: torch.Tensor    # int64 [S+1]
+    arrival: torch.Tensor    # int64 [N]
+    dist: torch.Tensor       # int32 [N]
+    true_bin: torch.Tensor   # int16 [N]
+    slo: torch.Tensor        # int64 [S]
+    bucket: torch.Tensor     # int32 [S]
+    num_buckets: int
+
+    def __post_init__(self):
+        _dev(self.offsets, torch.int64, "offsets")
+        _dev(self.arrival, torch.int64, "arrival")
+        _dev(self.dist, torch.int32, "dist")
+        _dev(self.true_bin, torch.int16, "true_bin")
+        _dev(self.slo, torch.int64, "slo")
+        _dev(self.bucket, torch.int32, "bucket")
+        self._c = _abi.TraceC(self.slo.numel(), self.offsets.data_ptr(), self.arrival.data_ptr(),
+                              self.dist.data_ptr(), self.true_bin.data_ptr(), self.slo.data_ptr(),
+                              self.bucket.data_ptr(), int(self.num_buckets))
+
+    @property
+    def num_scenarios(self):
+        return self.slo.numel()
+
+    @property
+    def num_arrivals(self):
+        return self.arrival.numel()
+
+    def validate(self, store: HistogramStore, stream=None):
+        _abi.check(_abi.lib().orloj_validate_trace(store.c(), ctypes.byref(self._c), _stream_ptr(stream)))
+
+    def c(self):
+        return ctypes.byref(self._c)
+
+
+def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, per_bucket=None,
+                 decision_log: bool | torch.Tensor = False, stream=None):
+    """Replay every scenario; returns (per_bucket int64 [num_buckets, 7], log or None).
+    per_bucket is ADDED to (pass a zeroed tensor to accumulate across calls)."""
+    dev = trace.arrival.device
+    if per_bucket is None:
+        per_bucket = torch.zeros((trace.num_buckets, 7), dtype=torch.int64, device=dev)
+    _dev(per_bucket, torch.int64, "per_bucket")
+    log = None
+    if isinstance(decision_log, torch.Tensor):
+        log = _dev(decision_log, torch.int32, "decision_log")
+    elif decision_log:
+        log = torch.zeros(trace.num_arrivals + trace.num_scenarios, dtype=torch.int32, device=dev)
+    _abi.check(_abi.lib().orloj_replay_trace(store.c(), profile.c(), trace.c(), per_bucket.data_ptr(), _ptr(log),
+                                             _stream_ptr(stream)))
+    return per_bucket, log

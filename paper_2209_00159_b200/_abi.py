@@ -1,0 +1,105 @@
+"""ctypes mirror of include/orloj.h and the loader for liborloj.so.
+
+Argument marshalling only: every step of the path runs in the CUDA library.
+There is no CPU fallback — if liborloj.so is missing or fails to load, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_PATH = os.path.join(PKG, "liborloj.so")
+HEADER = os.path.join(ROOT, "include", "orloj.h")
+
+NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+              "-shared", "-Xcompiler", "-fPIC"]
+
+STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "COLD_START", 3: "UNSORTED", 4: "CAPACITY", 5: "CUDA", 6: "OOM"}
+
+
+class OrlojError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"orloj {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def build(nvcc: str = "nvcc", verbose: bool = False) -> str:
+    src = os.path.join(PKG, "csrc", "orloj.cu")
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, src]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+class Store(ctypes.Structure):
+    _fields_ = [("num_dists", ctypes.c_int32), ("num_bins", ctypes.c_int32), ("bin_ticks", ctypes.c_int64),
+                ("log2_cdf", ctypes.c_void_p)]
+
+
+class LatencyProfile(ctypes.Structure):
+    _fields_ = [("kmax", ctypes.c_int32), ("offset_ticks", ctypes.c_void_p), ("ticks_per_bin", ctypes.c_void_p)]
+
+
+class QueuesC(ctypes.Structure):
+    _fields_ = [("num_queues", ctypes.c_int64), ("queue_offsets", ctypes.c_void_p),
+                ("arrival_ticks", ctypes.c_void_p), ("deadline_ticks", ctypes.c_void_p),
+                ("dist_id", ctypes.c_void_p), ("now_ticks", ctypes.c_void_p)]
+
+
+class TraceC(ctypes.Structure):
+    _fields_ = [("num_scenarios", ctypes.c_int64), ("arrival_offsets", ctypes.c_void_p),
+                ("arrival_ticks", ctypes.c_void_p), ("dist_id", ctypes.c_void_p), ("true_bin", ctypes.c_void_p),
+                ("slo_ticks", ctypes.c_void_p), ("bucket", ctypes.c_void_p), ("num_buckets", ctypes.c_int32)]
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("total", "finished", "dropped", "late", "batches", "busy_ticks", "span_ticks")]
+
+
+# symbol -> (restype, argtypes)
+_P = ctypes.c_void_p
+SIGNATURES = {
+    "orloj_last_error": (ctypes.c_char_p, []),
+    "orloj_abi_version": (ctypes.c_int32, []),
+    "orloj_store_build": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]),
+    "orloj_score_batches": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                           ctypes.POINTER(QueuesC), _P, _P, _P, _P]),
+    "orloj_pick_batch": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                        ctypes.POINTER(QueuesC), _P, _P, _P]),
+    "orloj_pick_batch_host_workspace": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64]),
+    "orloj_pick_batch_host": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int64,
+                                             _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "orloj_replay_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                          ctypes.POINTER(TraceC), _P, _P, _P]),
+    "orloj_validate_store": (ctypes.c_int, [ctypes.POINTER(Store), _P]),
+    "orloj_validate_queues": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC), _P]),
+    "orloj_validate_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(TraceC), _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load liborloj.so (fails loudly: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OrlojError(5, f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int):
+    if status != 0:
+        raise OrlojError(status, lib().orloj_last_error().decode())

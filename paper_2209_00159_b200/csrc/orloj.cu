@@ -1,0 +1,383 @@
+// orloj.cu — liborloj.so: the C ABI declared in include/orloj.h.
+//
+// Host side: O(1) argument validation, profile compilation (division magic),
+// template dispatch on (bins per lane, member slots), launches on the caller's
+// stream.  No allocation and no global mutable state in the hot calls.
+#include "../../include/orloj.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "replay_kernel.cuh"
+#include "score_kernel.cuh"
+#include "store_kernel.cuh"
+
+using namespace orloj;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+orloj_status fail(orloj_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+orloj_status cuda_fail(cudaError_t e, const char *where) {
+  return fail(ORLOJ_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+orloj_status ok() {
+  g_last_error.clear();
+  return ORLOJ_OK;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+orloj_status check_store(const orloj_store *st, int max_bins) {
+  if (!st) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store is NULL");
+  if (st->num_dists < 1) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store.num_dists=%d < 1", st->num_dists);
+  if (st->num_bins < 4 || st->num_bins % 4)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store.num_bins=%d must be a positive multiple of 4", st->num_bins);
+  if (st->num_bins > max_bins)
+    return fail(ORLOJ_ERR_CAPACITY, "store.num_bins=%d > %d", st->num_bins, max_bins);
+  if (!st->log2_cdf || !aligned16(st->log2_cdf))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store.log2_cdf must be a 16-byte aligned device pointer");
+  return ORLOJ_OK;
+}
+
+// Compile the profile into kernel parameters (A3, A14, horizon check).
+orloj_status compile_profile(const orloj_latency_profile *pr, int32_t B, int kcap, ProfileDev *out) {
+  if (!pr || !pr->offset_ticks || !pr->ticks_per_bin)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile or its arrays are NULL");
+  if (pr->kmax < 1) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile.kmax=%d < 1", pr->kmax);
+  if (pr->kmax > kcap) return fail(ORLOJ_ERR_CAPACITY, "profile.kmax=%d > %d", pr->kmax, kcap);
+  std::memset(out, 0, sizeof(*out));
+  out->kmax = pr->kmax;
+  out->B = B;
+  for (int k = 0; k < pr->kmax; ++k) {
+    const int64_t a = pr->offset_ticks[k], w = pr->ticks_per_bin[k];
+    if (a < 0 || w < 1)
+      return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile k=%d: need a_k >= 0 and w_k >= 1 (got %lld, %lld)", k + 1,
+                  (long long)a, (long long)w);
+    if (k > 0 && (a < pr->offset_ticks[k - 1] || w < pr->ticks_per_bin[k - 1]))
+      return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile must be non-decreasing in k (A14); violated at k=%d", k + 1);
+    if (a > 0x7fffffffLL || w > 0x7fffffffLL || a + w * (int64_t)B > 0x7fffffffLL)
+      return fail(ORLOJ_ERR_CAPACITY, "profile horizon a_k + w_k*B = %lld ticks exceeds 2^31-1 at k=%d",
+                  (long long)(a + w * (int64_t)B), k + 1);
+    uint32_t c = 0;
+    while ((1ull << c) < (uint64_t)w) ++c;
+    const uint64_t num = 1ull << (31 + c);
+    const uint64_t m = (num + (uint64_t)w - 1) / (uint64_t)w;
+    out->a[k] = (int32_t)a;
+    out->w[k] = (int32_t)w;
+    out->wB[k] = (int32_t)(w * B);
+    out->mag[k] = (uint32_t)m;
+    out->sh[k] = c;
+  }
+  return ORLOJ_OK;
+}
+
+orloj_status check_queues(const orloj_queues *q) {
+  if (!q) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "queues is NULL");
+  if (q->num_queues < 0) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "num_queues < 0");
+  if (q->num_queues > 0 && (!q->queue_offsets || !q->deadline_ticks || !q->dist_id || !q->now_ticks))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "queue arrays must be non-NULL device pointers");
+  return ORLOJ_OK;
+}
+
+int bins_per_lane(int B) { return B <= 32 ? 1 : B <= 64 ? 2 : B <= 128 ? 4 : 8; }
+int slots_for(int kmax) {
+  const int c = (kmax + 31) / 32;
+  return c <= 1 ? 1 : c <= 2 ? 2 : c <= 4 ? 4 : 8;
+}
+
+template <int BPL, int SLOTS, bool PICK, bool STREAM>
+cudaError_t launch_score_t(const ScoreParams &p, cudaStream_t s) {
+  const int64_t blocks = (p.Q + SCORE_WARPS - 1) / SCORE_WARPS;
+  score_kernel<BPL, SLOTS, PICK, STREAM><<<(unsigned)blocks, SCORE_WARPS * 32, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int BPL, bool PICK, bool STREAM>
+cudaError_t launch_score_s(const ScoreParams &p, int slots, cudaStream_t s) {
+  switch (slots) {
+    case 1: return launch_score_t<BPL, 1, PICK, STREAM>(p, s);
+    case 2: return launch_score_t<BPL, 2, PICK, STREAM>(p, s);
+    case 4: return launch_score_t<BPL, 4, PICK, STREAM>(p, s);
+    default: return launch_score_t<BPL, 8, PICK, STREAM>(p, s);
+  }
+}
+
+template <bool PICK>
+cudaError_t launch_score_b(const ScoreParams &p, bool stream, cudaStream_t s) {
+  const int slots = slots_for(p.kmax);
+  switch (bins_per_lane(p.B)) {
+    case 1: return launch_score_s<1, PICK, false>(p, slots, s);
+    case 2: return launch_score_s<2, PICK, false>(p, slots, s);
+    case 4: return launch_score_s<4, PICK, false>(p, slots, s);
+    default:
+      return stream ? launch_score_s<8, PICK, true>(p, slots, s) : launch_score_s<8, PICK, false>(p, slots, s);
+  }
+}
+
+// Rows streamed once (the per-request store of C3, larger than L2) bypass L1
+// and are evict-first in L2; small shared stores (a few applications) stay
+// cacheable.
+constexpr int64_t STREAM_STORE_BYTES = 256ll << 20;
+
+cudaError_t launch_score(const ScoreParams &p, bool pick, int64_t store_bytes, cudaStream_t s) {
+  const bool stream = store_bytes > STREAM_STORE_BYTES;
+  return pick ? launch_score_b<true>(p, stream, s) : launch_score_b<false>(p, stream, s);
+}
+
+orloj_status prepare_score(const orloj_store *store, const orloj_latency_profile *profile,
+                           const orloj_queues *queues, ScoreParams *p) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
+  if ((st = check_queues(queues))) return st;
+  std::memset(p, 0, sizeof(*p));
+  if ((st = compile_profile(profile, store->num_bins, ORLOJ_MAX_KMAX, &p->prof))) return st;
+  p->log2F = store->log2_cdf;
+  p->B = store->num_bins;
+  p->kmax = profile->kmax;
+  p->Q = queues->num_queues;
+  p->offsets = queues->queue_offsets;
+  p->deadline = queues->deadline_ticks;
+  p->dist = queues->dist_id;
+  p->now = queues->now_ticks;
+  return ORLOJ_OK;
+}
+
+int64_t store_bytes(const orloj_store *st) { return (int64_t)st->num_dists * st->num_bins * 4; }
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+orloj_status run_flag_check(unsigned int *dflag, cudaStream_t s, unsigned int *host_flag) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host_flag, dflag, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(dflag, s);
+  cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "validation");
+  return ORLOJ_OK;
+}
+
+orloj_status alloc_flag(unsigned int **dflag, cudaStream_t s) {
+  if (cudaMallocAsync((void **)dflag, sizeof(unsigned), s) != cudaSuccess)
+    return fail(ORLOJ_ERR_OOM, "cannot allocate validation scratch");
+  if (cudaMemsetAsync(*dflag, 0, sizeof(unsigned), s) != cudaSuccess)
+    return fail(ORLOJ_ERR_CUDA, "memset of validation scratch failed");
+  return ORLOJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *orloj_last_error(void) { return g_last_error.c_str(); }
+
+int32_t orloj_abi_version(void) { return ORLOJ_ABI_VERSION; }
+
+orloj_status orloj_store_build(const uint32_t *counts, int32_t D, int32_t B, float *out, void *stream) {
+  if (!counts || !out || D < 1 || B < 4 || B % 4)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store_build: need counts, out, D >= 1, B a positive multiple of 4");
+  if (B > ORLOJ_MAX_BINS) return fail(ORLOJ_ERR_CAPACITY, "store_build: B=%d > %d", B, ORLOJ_MAX_BINS);
+  if (!aligned16(out)) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store_build: out must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned int *dflag;
+  orloj_status st = alloc_flag(&dflag, s);
+  if (st) return st;
+  const int64_t threads = (int64_t)D * 32;
+  store_build_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(counts, D, B, out, dflag);
+  unsigned int hf = 0;
+  if ((st = run_flag_check(dflag, s, &hf))) return st;
+  if (hf) return fail(ORLOJ_ERR_COLD_START, "store_build: a histogram has total count 0 (cold start)");
+  return ok();
+}
+
+orloj_status orloj_score_batches(const orloj_store *store, const orloj_latency_profile *profile,
+                                 const orloj_queues *queues, float *E, float *P, float *EL, void *stream) {
+  ScoreParams p;
+  orloj_status st = prepare_score(store, profile, queues, &p);
+  if (st) return st;
+  if (!E && !P && !EL) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "score_batches: no output requested");
+  p.E = E;
+  p.P = P;
+  p.EL = EL;
+  if (p.Q == 0) return ok();
+  cudaError_t e = launch_score(p, false, store_bytes(store), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "score_batches launch");
+  return ok();
+}
+
+orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_profile *profile,
+                              const orloj_queues *queues, int32_t *best_k, float *best_E, void *stream) {
+  ScoreParams p;
+  orloj_status st = prepare_score(store, profile, queues, &p);
+  if (st) return st;
+  if (!best_k || !best_E) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch: best_k / best_expected NULL");
+  p.best_k = best_k;
+  p.best_E = best_E;
+  if (p.Q == 0) return ok();
+  cudaError_t e = launch_score(p, true, store_bytes(store), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "pick_batch launch");
+  return ok();
+}
+
+size_t orloj_pick_batch_host_workspace(int64_t Q, int64_t N) {
+  if (Q < 0 || N < 0) return 0;
+  return align256((Q + 1) * 8) + align256(N * 8) + align256(N * 4) + align256(Q * 8) + align256(Q * 4) +
+         align256(Q * 4);
+}
+
+orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency_profile *profile, int64_t Q,
+                                   const int64_t *off_h, const int64_t *dl_h, const int32_t *dist_h,
+                                   const int64_t *now_h, int32_t *bk_h, float *bE_h, void *ws, size_t ws_bytes,
+                                   void *stream) {
+  if (Q < 0 || !off_h || (Q > 0 && (!now_h || !bk_h || !bE_h)))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: bad host arrays");
+  const int64_t N = off_h[Q];
+  if (N < 0 || (N > 0 && (!dl_h || !dist_h)))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: bad member arrays");
+  if (!ws || ((uintptr_t)ws & 255u) || ws_bytes < orloj_pick_batch_host_workspace(Q, N))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: workspace too small or misaligned");
+  char *w = (char *)ws;
+  int64_t *off_d = (int64_t *)w;  w += align256((Q + 1) * 8);
+  int64_t *dl_d = (int64_t *)w;   w += align256(N * 8);
+  int32_t *dist_d = (int32_t *)w; w += align256(N * 4);
+  int64_t *now_d = (int64_t *)w;  w += align256(Q * 8);
+  int32_t *bk_d = (int32_t *)w;   w += align256(Q * 4);
+  float *bE_d = (float *)w;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(off_d, off_h, (Q + 1) * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && N) e = cudaMemcpyAsync(dl_d, dl_h, N * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && N) e = cudaMemcpyAsync(dist_d, dist_h, N * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && Q) e = cudaMemcpyAsync(now_d, now_h, Q * 8, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "pick_batch_host H2D");
+  orloj_queues q{Q, off_d, nullptr, dl_d, dist_d, now_d};
+  orloj_status st = orloj_pick_batch(store, profile, &q, bk_d, bE_d, stream);
+  if (st) return st;
+  if (Q) {
+    e = cudaMemcpyAsync(bk_h, bk_d, Q * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bE_h, bE_d, Q * 4, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "pick_batch_host D2H");
+  }
+  return ok();
+}
+
+orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
+                                const orloj_trace *tr, orloj_counters *per_bucket, int32_t *log, void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
+  if (!tr || tr->num_scenarios < 0 || tr->num_buckets < 1)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace: need num_scenarios >= 0 and num_buckets >= 1");
+  if (tr->num_scenarios > 0 && (!tr->arrival_offsets || !tr->arrival_ticks || !tr->dist_id || !tr->true_bin ||
+                                !tr->slo_ticks || !tr->bucket || !per_bucket))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace arrays / per_bucket must be non-NULL device pointers");
+  ReplayParams p;
+  std::memset(&p, 0, sizeof(p));
+  if ((st = compile_profile(profile, store->num_bins, ORLOJ_REPLAY_MAX_KMAX, &p.prof))) return st;
+  const int B = store->num_bins, D = store->num_dists;
+  const int bpl = bins_per_lane(B);
+  const size_t store_b = (size_t)D * B * 4;
+  if (store_b > (64u << 10))
+    return fail(ORLOJ_ERR_CAPACITY, "replay: store of %zu bytes exceeds the 64 KiB shared-memory budget", store_b);
+  const size_t warp_b = (size_t)(2 * (32 * bpl + 4) + 32) * 4;
+  const size_t smem = store_b + (size_t)((D + 3) & ~3) * 4 + REPLAY_WARPS * warp_b;
+  p.log2F = store->log2_cdf;
+  p.D = D;
+  p.B = B;
+  p.S = tr->num_scenarios;
+  p.arr_off = tr->arrival_offsets;
+  p.arrival = tr->arrival_ticks;
+  p.dist = tr->dist_id;
+  p.true_bin = tr->true_bin;
+  p.slo = tr->slo_ticks;
+  p.bucket = tr->bucket;
+  p.counters = reinterpret_cast<unsigned long long *>(per_bucket);
+  p.log = log;
+  if (p.S == 0) return ok();
+  const unsigned blocks = (unsigned)((p.S + REPLAY_WARPS - 1) / REPLAY_WARPS);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  switch (bpl) {
+    case 1:
+      e = cudaFuncSetAttribute(replay_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) replay_kernel<1><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);
+      break;
+    case 2:
+      e = cudaFuncSetAttribute(replay_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) replay_kernel<2><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);
+      break;
+    default:
+      e = cudaFuncSetAttribute(replay_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess) replay_kernel<4><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);
+      break;
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "replay_trace launch");
+  return ok();
+}
+
+orloj_status orloj_validate_store(const orloj_store *store, void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned int *dflag;
+  if ((st = alloc_flag(&dflag, s))) return st;
+  validate_store_kernel<<<148 * 8, 256, 0, s>>>(store->log2_cdf, store->num_dists, store->num_bins, dflag);
+  unsigned hf = 0;
+  if ((st = run_flag_check(dflag, s, &hf))) return st;
+  if (hf) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store rows must be non-decreasing, <= 0, and end with 0.0f");
+  return ok();
+}
+
+orloj_status orloj_validate_queues(const orloj_store *store, const orloj_queues *q, void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
+  if ((st = check_queues(q))) return st;
+  if (q->num_queues == 0) return ok();
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned int *dflag;
+  if ((st = alloc_flag(&dflag, s))) return st;
+  validate_queues_kernel<<<148 * 8, 256, 0, s>>>(q->queue_offsets, q->num_queues, q->arrival_ticks,
+                                                  q->deadline_ticks, q->dist_id, store->num_dists, dflag);
+  unsigned hf = 0;
+  if ((st = run_flag_check(dflag, s, &hf))) return st;
+  if (hf & 1u) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "queues: bad offsets or dist_id out of range");
+  if (hf & 2u) return fail(ORLOJ_ERR_UNSORTED, "queues: members not in (deadline, arrival, index) order");
+  return ok();
+}
+
+orloj_status orloj_validate_trace(const orloj_store *store, const orloj_trace *tr, void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
+  if (!tr || tr->num_scenarios < 0 || tr->num_buckets < 1)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace: need num_scenarios >= 0 and num_buckets >= 1");
+  if (tr->num_scenarios == 0) return ok();
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned int *dflag;
+  if ((st = alloc_flag(&dflag, s))) return st;
+  validate_trace_kernel<<<148 * 8, 256, 0, s>>>(tr->arrival_offsets, tr->num_scenarios, tr->arrival_ticks,
+                                                 tr->dist_id, tr->true_bin, tr->slo_ticks, tr->bucket,
+                                                 tr->num_buckets, store->num_dists, store->num_bins, dflag);
+  unsigned hf = 0;
+  if ((st = run_flag_check(dflag, s, &hf))) return st;
+  if (hf & 1u) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace: offsets / ids / bins / buckets / slo out of range");
+  if (hf & 2u) return fail(ORLOJ_ERR_UNSORTED, "trace: arrivals not non-decreasing within a scenario");
+  return ok();
+}
+
+}  // extern "C"

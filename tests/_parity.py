@@ -1,0 +1,58 @@
+"""Parity helpers for the GPU tests (test infrastructure: may use the oracle)."""
+import numpy as np
+
+import oracle
+
+P_TOL = 1e-5          # north star: probabilities within 1e-5 absolute
+
+
+def e_tol(kmax):
+    """E_k within 1e-5 * k (SURVEY §8(c) tolerances; derivation DESIGN.md §5)."""
+    return 1e-5 * np.arange(1, kmax + 1)
+
+
+def oracle_score(counts, prof_a, prof_w, q, want_P=False, want_EL=False):
+    return oracle.score(oracle.cdf(counts), prof_a, prof_w, q.offsets, q.deadline, q.dist, q.now,
+                        want_P=want_P, want_EL=want_EL)
+
+
+def check_E(E_gpu, E_or, lens, kmax):
+    """Element-wise E parity; entries k > K_q must be exactly 0."""
+    K = np.minimum(lens, kmax)
+    err = np.abs(E_gpu.astype(np.float64) - E_or)
+    assert (err <= e_tol(kmax)[None, :] + 1e-7).all(), f"max E err {err.max()}"
+    mask = np.arange(1, kmax + 1)[None, :] > K[:, None]
+    assert (E_gpu[mask] == 0).all()
+    return err.max()
+
+
+def check_pick(bk_gpu, bE_gpu, E_gpu, E_or, bk_or, lens, kmax):
+    """k* bit-exact except documented ties: k_g != k_o is accepted iff
+    E_or[k_o] - E_or[k_g] <= |E_gpu[k_g] - E_or[k_g]| + |E_gpu[k_o] - E_or[k_o]|,
+    each error within 1e-5 k.  Returns the number of ties."""
+    K = np.minimum(lens, kmax)
+    assert ((bk_gpu == 0) == (K == 0)).all()
+    ties = 0
+    for q in np.nonzero(bk_gpu != bk_or)[0]:
+        kg, ko = int(bk_gpu[q]), int(bk_or[q])
+        eg = abs(float(E_gpu[q, kg - 1]) - E_or[q, kg - 1])
+        eo = abs(float(E_gpu[q, ko - 1]) - E_or[q, ko - 1])
+        assert eg <= 1e-5 * kg + 1e-7 and eo <= 1e-5 * ko + 1e-7
+        assert E_or[q, ko - 1] - E_or[q, kg - 1] <= eg + eo + 1e-12, f"queue {q}: k_gpu={kg} k_oracle={ko}"
+        ties += 1
+    nz = K > 0
+    # best_E is E_gpu[k*] (pick and score variants evaluate the same arithmetic)
+    idx = np.nonzero(nz)[0]
+    assert (bE_gpu[idx] == E_gpu[idx, bk_gpu[idx] - 1]).all()
+    assert (bE_gpu[~nz] == 0).all()
+    return ties
+
+
+def check_P(P_gpu, P_or, lens, kmax):
+    K = np.minimum(lens, kmax)
+    tri = np.concatenate([np.full(k, k) for k in range(1, kmax + 1)])  # k of each packed entry
+    valid = tri[None, :] <= K[:, None]
+    err = np.abs(P_gpu.astype(np.float64) - P_or)[valid]
+    assert err.size == 0 or err.max() <= P_TOL, f"max P err {err.max()}"
+    assert (P_gpu[valid] >= 0).all() and (P_gpu[valid] <= 1).all()
+    return 0.0 if err.size == 0 else err.max()
