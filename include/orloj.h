@@ -59,7 +59,7 @@ typedef enum {
   ORLOJ_ERR_INVALID_ARGUMENT = 1, /* bad pointer / size / profile (non-monotone, w_k < 1, ...) */
   ORLOJ_ERR_COLD_START = 2,       /* a histogram has total count 0 */
   ORLOJ_ERR_UNSORTED = 3,         /* queue / trace order violated (validation only) */
-  ORLOJ_ERR_CAPACITY = 4,         /* beyond built limits (kmax, B, 2^31-tick horizon, store size) */
+  ORLOJ_ERR_CAPACITY = 4,         /* beyond built limits (kmax, B, 2^30-tick horizon, store size) */
   ORLOJ_ERR_CUDA = 5,             /* CUDA runtime / launch error */
   ORLOJ_ERR_OOM = 6               /* scratch allocation failed (validation / store build only) */
 } orloj_status;
@@ -106,8 +106,9 @@ typedef struct {
 /* The table is copied into kernel parameters at each call (host pointers need
  * only be valid during the call).  Monotonicity (A14) is required
  * (INVALID_ARGUMENT otherwise): it makes P_r(k+1) <= P_r(k) hold bit-exactly.
- * Horizon: a_kmax + w_kmax * B must be <= 2^31 - 1 ticks (CAPACITY otherwise),
- * so bin lookups run in exact 32-bit integer arithmetic. */
+ * Horizon: a_kmax + w_kmax * B must be <= 2^30 - 1 ticks (~17.9 min at 1 us
+ * ticks; CAPACITY otherwise), so bin lookups run in exact 32-bit integer
+ * arithmetic on doubled slacks. */
 
 /* ---------------------------------------------------------------------------
  * Queues (release time, deadline = release + SLO, and an

@@ -12,7 +12,7 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "liborloj.so")
+LIB_PATH = os.environ.get("ORLOJ_LIB") or os.path.join(PKG, "liborloj.so")
 HEADER = os.path.join(ROOT, "include", "orloj.h")
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

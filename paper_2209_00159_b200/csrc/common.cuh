@@ -11,37 +11,41 @@ constexpr int KCAP = 256;          // ORLOJ_MAX_KMAX
 constexpr unsigned FULL = 0xffffffffu;
 
 // Latency profile as kernel parameters (constant bank; stream-safe, no global
-// state).  For every k: a_k, w_k, w_k*B and the exact 32-bit division magic for
-// floor(x / w_k), 0 <= x < 2^31 (see lookup_bin).  Index k-1.
+// state).  For every k (index k-1): a_k, w_k, and for the bin lookup the
+// doubled offsets 2 a_k, 2 w_k B and the exact division magic (mag, sh) for
+// floor(x / w_k), 0 <= x < 2^30 (see lookup_bin).
 struct ProfileDev {
   int32_t kmax;
   int32_t B;
   int32_t a[KCAP];
   int32_t w[KCAP];
-  int32_t wB[KCAP];
+  int32_t a2[KCAP];
+  int32_t wB2[KCAP];
   uint32_t mag[KCAP];
   uint32_t sh[KCAP];
 };
 
-// sigma = D_r - t clamped into int32: below 0 every lookup gives bin 0, above
-// the horizon (a_kmax + w_kmax*B <= 2^31-1, checked on the host) every lookup
-// saturates at B, so the clamp never changes a result.
-__device__ __forceinline__ int32_t clamp_sigma(int64_t sigma) {
-  sigma = sigma < -1 ? -1 : sigma;
-  sigma = sigma > 0x7fffffffLL ? 0x7fffffffLL : sigma;
-  return (int32_t)sigma;
+// Slack sigma = D_r - t, clamped to [0, 2^30 - 1] and doubled.  Clamping below
+// at 0 changes nothing (floor(x / w) = 0 for every x < w, and x = sigma - a_k
+// <= 0 there); above, the horizon a_kmax + w_kmax B <= 2^30 - 1 (checked on the
+// host) makes every lookup saturate at B already.
+__device__ __forceinline__ int32_t sigma2(int64_t sigma) {
+  sigma = sigma < 0 ? 0 : sigma;
+  sigma = sigma > 0x3fffffffLL ? 0x3fffffffLL : sigma;
+  return (int32_t)(2 * sigma);
 }
 
-// Eq. 3-4 + Eq. 9 (CDF form): i*(r,k) = clamp(floor((sigma - a_k) / w_k), 0, B).
-// x = min(sigma - a_k, w_k*B) < 2^31; floor(x / w) = umulhi(2x, m) >> c with
-// c = ceil(log2 w), m = ceil(2^(31+c) / w) < 2^32 — exact for every such x
-// (x * (m*w - 2^(31+c)) < 2^31 * w <= 2^(31+c)).  Integer, bit-exact.
-__device__ __forceinline__ int32_t lookup_bin(int32_t sig, int32_t a, int32_t wB, uint32_t mag,
+// Eq. 3-4 + Eq. 9 (CDF form): i*(r,k) = clamp(floor((sigma - a_k) / w_k), 0, B)
+// from s2 = 2 sigma:  x2 = clamp(s2 - 2 a_k, 0, 2 w_k B) = 2x,  and
+// floor(x / w) = umulhi(2x, m) >> c with c = ceil(log2 w), m = ceil(2^(31+c) / w)
+// < 2^32 — exact for every 0 <= x < 2^31 since x (m w - 2^(31+c)) < 2^31 w <=
+// 2^(31+c).  Four integer instructions, bit-exact.
+__device__ __forceinline__ int32_t lookup_bin(int32_t s2, int32_t a2, int32_t wB2, uint32_t mag,
                                               uint32_t sh) {
-  int32_t x = sig - a;
-  x = x < wB ? x : wB;
-  uint32_t q = __umulhi((uint32_t)x << 1, mag) >> sh;
-  return x < 0 ? 0 : (int32_t)q;
+  int32_t x2 = s2 - a2;
+  x2 = x2 < wB2 ? x2 : wB2;
+  x2 = x2 > 0 ? x2 : 0;
+  return (int32_t)(__umulhi((uint32_t)x2, mag) >> sh);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -75,39 +79,26 @@ __device__ __forceinline__ float bfly_push(float (&pend)[5], float v, int j, int
   return v;
 }
 
-// A lane's bins as one vector register group: V = 1, 2, 4 or 8 floats
-// (V = 8 is one 256-bit load, new on sm_100).
+// A lane's bins: NV vectors of V floats (V = min(BPL, 4)).  Vector v of lane l
+// covers floats [(32 v + l) V, +V) of a row, so each vector load / store of a
+// warp is one contiguous, conflict-free 32 V-byte-per-lane sweep.
 template <int V> struct alignas(4 * V) Vec {
   float x[V];
 };
 
-// Row loads of V floats at p (aligned to 4V bytes).  STREAM: rows read exactly
-// once (the per-request store of C3) bypass L1 and are marked evict-first in
-// L2.  `half` (V = 8 only): only the first 4 floats exist (B % 8 == 4 tail).
+// Row loads of V floats (aligned to 4V bytes).  STREAM: rows read exactly once
+// (the per-request store of C3) bypass L1.
 template <int V, bool STREAM>
-__device__ __forceinline__ Vec<V> ldrow(const float *p, bool half = false) {
+__device__ __forceinline__ Vec<V> ldrow(const float *p) {
   Vec<V> r;
-  if constexpr (V == 8) {
-    if (!half) {
-      if constexpr (STREAM)
-        asm volatile(
-            "ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]),
-              "=f"(r.x[6]), "=f"(r.x[7])
-            : "l"(p));
-      else
-        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
-                       "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
-                     : "l"(p));
+  if constexpr (V == 4) {
+    if constexpr (STREAM) {
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]) : "l"(p));
     } else {
-      const float4 lo = __ldg(reinterpret_cast<const float4 *>(p));
-      r.x[0] = lo.x; r.x[1] = lo.y; r.x[2] = lo.z; r.x[3] = lo.w;
-      r.x[4] = r.x[5] = r.x[6] = r.x[7] = 0.f;
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+      r.x[0] = v.x; r.x[1] = v.y; r.x[2] = v.z; r.x[3] = v.w;
     }
-  } else if constexpr (V == 4) {
-    const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
-    r.x[0] = v.x; r.x[1] = v.y; r.x[2] = v.z; r.x[3] = v.w;
   } else if constexpr (V == 2) {
     const float2 v = __ldg(reinterpret_cast<const float2 *>(p));
     r.x[0] = v.x; r.x[1] = v.y;
@@ -125,18 +116,105 @@ __device__ __forceinline__ Vec<V> vzero() {
   return z;
 }
 
-// Store V floats to shared memory as 128-bit (or narrower) stores.
+// Store V floats (V <= 4) to shared memory as one vector store.
 template <int V>
-__device__ __forceinline__ void st_stage(float *dst, const float (&v)[V]) {
-  if constexpr (V >= 4) {
-#pragma unroll
-    for (int h = 0; h < V; h += 4)
-      *reinterpret_cast<float4 *>(dst + h) = make_float4(v[h], v[h + 1], v[h + 2], v[h + 3]);
+__device__ __forceinline__ void st_vec(float *dst, const float *v) {
+  if constexpr (V == 4) {
+    *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
   } else if constexpr (V == 2) {
     *reinterpret_cast<float2 *>(dst) = make_float2(v[0], v[1]);
   } else {
     dst[0] = v[0];
   }
+}
+
+// Warp-uniform copy of a value that is equal across the warp: REDUX writes a
+// uniform register, so branches on it compile to uniform branches (no
+// BSSY / BSYNC reconvergence bookkeeping).
+__device__ __forceinline__ int warp_uniform(int x) {
+  return (int)__reduce_max_sync(FULL, (unsigned)x);
+}
+
+// ---- bulk async copies (TMA engine, cp.async.bulk) + mbarriers -------------
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// 32-bit shared-space load (the address already includes the buffer base).
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+// Make mbarrier initialisation visible to the async proxy.  CTA-local barriers
+// only need the proxy fence; the cluster-scope fence.mbarrier_init also flushes
+// L1 (CCTL.IVALL), which every warp of this kernel would pay.
+__device__ __forceinline__ void mbar_init_fence() {
+#ifdef ORLOJ_CLUSTER_INIT_FENCE
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#else
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+}
+
+// Wait until the phase with parity `phase` of the barrier has completed.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+// Order this thread's earlier generic-proxy shared-memory accesses before
+// subsequent async-proxy (bulk copy) writes to the same buffer.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Bulk copy of `bytes` (multiple of 16, 16-B aligned both sides) from global to
+// shared memory completing on `bar`, issued only where `pred` is set (one lane
+// per warp) — predicated, so the warp does not diverge.
+template <bool STREAM>
+__device__ __forceinline__ void bulk_row(bool pred, uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                                         uint64_t pol) {
+  if constexpr (STREAM)
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %5, 0;\n"
+        " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4; }" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol), "r"((int)pred)
+        : "memory");
+  else
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+        " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3]; }" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "r"((int)pred)
+        : "memory");
+}
+
+// Arm `bar` for `bytes` of incoming bulk copies (predicated like bulk_row),
+// after ordering earlier generic shared-memory reads of the refilled buffer
+// before the async-proxy writes.
+__device__ __forceinline__ void arm_barrier(bool pred, uint32_t bar, uint32_t bytes) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %2, 0;\n"
+      " @p fence.proxy.async.shared::cta;\n"
+      " @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1; }" ::"r"(bar),
+      "r"(bytes), "r"((int)pred)
+      : "memory");
 }
 
 }  // namespace orloj

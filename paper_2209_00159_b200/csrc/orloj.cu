@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -73,8 +74,8 @@ orloj_status compile_profile(const orloj_latency_profile *pr, int32_t B, int kca
                   (long long)a, (long long)w);
     if (k > 0 && (a < pr->offset_ticks[k - 1] || w < pr->ticks_per_bin[k - 1]))
       return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile must be non-decreasing in k (A14); violated at k=%d", k + 1);
-    if (a > 0x7fffffffLL || w > 0x7fffffffLL || a + w * (int64_t)B > 0x7fffffffLL)
-      return fail(ORLOJ_ERR_CAPACITY, "profile horizon a_k + w_k*B = %lld ticks exceeds 2^31-1 at k=%d",
+    if (a > 0x3fffffffLL || w > 0x3fffffffLL || a + w * (int64_t)B > 0x3fffffffLL)
+      return fail(ORLOJ_ERR_CAPACITY, "profile horizon a_k + w_k*B = %lld ticks exceeds 2^30-1 at k=%d",
                   (long long)(a + w * (int64_t)B), k + 1);
     uint32_t c = 0;
     while ((1ull << c) < (uint64_t)w) ++c;
@@ -82,7 +83,8 @@ orloj_status compile_profile(const orloj_latency_profile *pr, int32_t B, int kca
     const uint64_t m = (num + (uint64_t)w - 1) / (uint64_t)w;
     out->a[k] = (int32_t)a;
     out->w[k] = (int32_t)w;
-    out->wB[k] = (int32_t)(w * B);
+    out->a2[k] = (int32_t)(2 * a);
+    out->wB2[k] = (int32_t)(2 * w * B);
     out->mag[k] = (uint32_t)m;
     out->sh[k] = c;
   }
@@ -106,7 +108,15 @@ int slots_for(int kmax) {
 template <int BPL, int SLOTS, bool PICK, bool STREAM>
 cudaError_t launch_score_t(const ScoreParams &p, cudaStream_t s) {
   const int64_t blocks = (p.Q + SCORE_WARPS - 1) / SCORE_WARPS;
-  score_kernel<BPL, SLOTS, PICK, STREAM><<<(unsigned)blocks, SCORE_WARPS * 32, 0, s>>>(p);
+  const size_t smem = ScoreShape<BPL>::smem_bytes();
+  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
+  if (!configured.load(std::memory_order_acquire)) {
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<BPL, SLOTS, PICK, STREAM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_release);
+  }
+  score_kernel<BPL, SLOTS, PICK, STREAM><<<(unsigned)blocks, SCORE_WARPS * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -212,11 +222,11 @@ orloj_status orloj_score_batches(const orloj_store *store, const orloj_latency_p
   ScoreParams p;
   orloj_status st = prepare_score(store, profile, queues, &p);
   if (st) return st;
+  if (p.Q == 0) return ok();
   if (!E && !P && !EL) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "score_batches: no output requested");
   p.E = E;
   p.P = P;
   p.EL = EL;
-  if (p.Q == 0) return ok();
   cudaError_t e = launch_score(p, false, store_bytes(store), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "score_batches launch");
   return ok();
@@ -227,10 +237,10 @@ orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_prof
   ScoreParams p;
   orloj_status st = prepare_score(store, profile, queues, &p);
   if (st) return st;
+  if (p.Q == 0) return ok();
   if (!best_k || !best_E) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch: best_k / best_expected NULL");
   p.best_k = best_k;
   p.best_E = best_E;
-  if (p.Q == 0) return ok();
   cudaError_t e = launch_score(p, true, store_bytes(store), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "pick_batch launch");
   return ok();

@@ -82,7 +82,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int64_t *arr = p.arrival + base;
   const int32_t *dis = p.dist + base;
   const int16_t *tbs = p.true_bin + base;
-  const int32_t a1 = p.prof.a[0], wB1 = p.prof.wB[0];
+  const int32_t a21 = p.prof.a2[0], wB21 = p.prof.wB2[0];
   const uint32_t mg1 = p.prof.mag[0], sh1 = p.prof.sh[0];
 
   int64_t t = INT64_MIN;
@@ -103,7 +103,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const int r = valid ? s_win[carry_off + lane] : 0;
       bool keep = false;
       if (valid) {
-        const int32_t i1 = lookup_bin(clamp_sigma(arr[r] + slo - t), a1, wB1, mg1, sh1);
+        const int32_t i1 = lookup_bin(sigma2(arr[r] + slo - t), a21, wB21, mg1, sh1);
         keep = i1 >= s_mmin[dis[r]];
       }
       const unsigned vm = __ballot_sync(FULL, valid);
@@ -120,7 +120,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       if (vm == 0) break;
       bool keep = false;
       if (valid) {
-        const int32_t i1 = lookup_bin(clamp_sigma(arr[idx] + slo - t), a1, wB1, mg1, sh1);
+        const int32_t i1 = lookup_bin(sigma2(arr[idx] + slo - t), a21, wB21, mg1, sh1);
         keep = i1 >= s_mmin[dis[idx]];
       }
       const unsigned km = __ballot_sync(FULL, keep);
@@ -143,6 +143,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
     ncarry = 0;
     carry_off = 0;
+    wc = warp_uniform(wc);
     __syncwarp();
     if (wc == 0) continue;
 
@@ -150,7 +151,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     const bool mem = lane < wc;
     const int r = mem ? s_win[lane] : 0;
     const int64_t Dr = mem ? arr[r] + slo : 0;
-    const int32_t sig = mem ? clamp_sigma(Dr - t) : -1;
+    const int32_t sig = mem ? sigma2(Dr - t) : 0;
     const int dr = mem ? dis[r] : 0;
     const int tb = mem ? (int)tbs[r] : 0;
 
@@ -170,10 +171,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
           for (int e = 0; e < BPL; ++e) lg[e] += x.x[e];
         }
         float *sg = (kk & 1) ? stg1 : stg0;
-        st_stage<BPL>(sg + lane * BPL, lg);
+        st_vec<BPL>(sg + lane * BPL, lg);
         __syncwarp();
         if (lane <= kk) {
-          const int i = lookup_bin(sig, p.prof.a[kk], p.prof.wB[kk], p.prof.mag[kk], p.prof.sh[kk]);
+          const int i = lookup_bin(sig, p.prof.a2[kk], p.prof.wB2[kk], p.prof.mag[kk], p.prof.sh[kk]);
           v[kk] = ex2_approx(sg[i - 1]);
         }
       }

@@ -7,14 +7,21 @@
 //   P_r(k)   = 2^{LG_k[i*]}  (0 when i* = 0)               (step SLO cost)
 //   E_k      = sum_{r<k} P_r(k);  k* = smallest argmax
 //
-// Layout: lane `l` owns bins [l*BPL, l*BPL + BPL) of the running LG in
-// registers (one 32-byte load per row at B = 256); member r lives in lane r % 32,
-// slot r / 32.  Per k the lane adds row d_k (prefetched PF rows ahead into a
-// register ring — up to PF*BPL*4 bytes in flight per lane), stages LG_k in a
-// double-buffered shared-memory row (index -1 holds -inf for i* = 0), then
-// every member r < k gathers LG_k[i*-1] and applies ex2.  The 32 per-lane
-// partial sums of a chunk of 32 consecutive k are reduced with the
-// transposing butterfly (31 shuffles per 32 k), leaving E_k in lane (k-1) % 32.
+// Row pipeline: every warp owns a ring of R shared-memory slots; one elected
+// lane streams the queue's rows log2F[d_k] into it with bulk async copies (the
+// TMA engine, cp.async.bulk + mbarrier complete_tx), R rows ahead — R KB in
+// flight per warp without holding registers.  Each slot is also the staging
+// row: lane l adds its bins of row k into its running LG (registers) and writes
+// LG_k back over the same slot, so after one __syncwarp every member can gather
+// LG_k[i*] from it.  The slot is refilled one iteration later.  A 16-byte head
+// before every slot holds -inf for i* = 0.
+//
+// Layout: lane l owns BPL bins as NV vectors of V = min(BPL, 4) floats, vector v
+// covering bins [(32 v + l) V, +V): conflict-free vector shared-memory accesses.
+// Member r lives in lane r % 32, slot r / 32.  The 32 per-lane partial sums of a
+// chunk of 32 consecutive k are reduced with the transposing butterfly (31
+// shuffles per 32 k), leaving E_k in lane (k-1) % 32.  K is made warp-uniform
+// (REDUX) so the member-slot switch compiles to uniform branches.
 #pragma once
 #include "common.cuh"
 
@@ -39,60 +46,88 @@ struct ScoreParams {
 
 constexpr int SCORE_WARPS = 8;
 
+#ifndef ORLOJ_RING
+#define ORLOJ_RING 8
+#endif
+
+template <int BPL>
+struct ScoreShape {
+  static constexpr int R = ORLOJ_RING;         // ring slots per warp (two groups of G rows)
+  static constexpr int G = R / 2;              // rows per barrier group; divides 32
+  static constexpr int SLOT = 32 * BPL + 4;    // floats per slot incl. the 16-B head
+  static constexpr size_t smem_bytes() { return (size_t)SCORE_WARPS * (R * SLOT * 4 + 2 * 8); }
+};
+
 template <int BPL, int SLOTS, bool PICK, bool STREAM>
 __global__ void __launch_bounds__(SCORE_WARPS * 32)
 score_kernel(const __grid_constant__ ScoreParams p) {
-  constexpr int BPAD = 32 * BPL;
-  constexpr int STG = BPAD + 4;             // 4-float head keeps rows 16-B aligned; [3] = -inf
-  constexpr int PF = BPL == 8 ? 4 : 8;      // rows in flight per warp
+  constexpr int V = BPL < 4 ? BPL : 4;      // floats per vector
+  constexpr int NV = BPL / V;               // vectors per lane per row
+  constexpr int R = ScoreShape<BPL>::R;
+  constexpr int G = ScoreShape<BPL>::G;
+  constexpr int SLOT = ScoreShape<BPL>::SLOT;
 
-  __shared__ __align__(16) float s_stage[SCORE_WARPS][2][STG];
-
+  extern __shared__ __align__(16) float s_dyn[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
+  float *ring = s_dyn + wid * (R * SLOT);                       // slot j: ring + j*SLOT, row at +4
+  uint64_t *bars = reinterpret_cast<uint64_t *>(s_dyn + SCORE_WARPS * R * SLOT) + wid * 2;
+
   const int64_t q = (int64_t)blockIdx.x * SCORE_WARPS + wid;
   if (q >= p.Q) return;
-
-  float *stg[2] = {&s_stage[wid][0][4], &s_stage[wid][1][4]};
-  if (lane == 0) {
-    stg[0][-1] = -INFINITY;
-    stg[1][-1] = -INFINITY;
-  }
 
   const int B = p.B;
   const int kmax = p.kmax;
   const int64_t off = p.offsets[q];
   const int64_t n = p.offsets[q + 1] - off;
-  const int K = (int)(n < kmax ? n : kmax);
+  const int K = warp_uniform((int)(n < kmax ? n : kmax));
   const int64_t now = p.now[q];
   const int64_t *dl = p.deadline + off;
   const int32_t *ids = p.dist + off;
+  const uint32_t row_bytes = (uint32_t)B * 4u;
+  const uint32_t ring_s = smem_addr(ring);
+  const uint32_t bar_s = smem_addr(bars);
+  const uint64_t pol = STREAM ? l2_evict_first_policy() : 0;
 
-  // sigma of the members this lane owns
+  int id_cur = lane < K ? ids[lane] : 0;
+  int id_nxt = 32 + lane < K ? ids[32 + lane] : 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) ring[j * SLOT + 3] = -INFINITY;
+    mbar_init(bar_s, 1);
+    mbar_init(bar_s + 8, 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  // prologue: rows 0 .. R-1 in two barrier groups
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    const int nrows = min(max(K - g * G, 0), G);
+    arm_barrier(lane == 0 && nrows > 0, bar_s + 8 * g, (uint32_t)nrows * row_bytes);
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int j = g * G + i;
+      const int d = __shfl_sync(FULL, id_cur, j);
+      bulk_row<STREAM>(lane == 0 && j < K, ring_s + (j * SLOT + 4) * 4, p.log2F + (int64_t)d * B, row_bytes,
+                       bar_s + 8 * g, pol);
+    }
+  }
+
+  // doubled slack of the members this lane owns; 0 (-> bin 0 -> P = 0) beyond K
   int32_t sig[SLOTS];
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     const int r = 32 * s + lane;
-    sig[s] = r < K ? clamp_sigma(dl[r] - now) : -1;
+    sig[s] = r < K ? sigma2(dl[r] - now) : 0;
   }
 
-  // bins this lane owns: [lane*BPL, lane*BPL + BPL) (B % 8 == 4: the last lane's half)
-  const bool vok = lane * BPL < B;
-  const bool vhalf = lane * BPL + BPL > B;
-  const float *myrow = p.log2F + lane * BPL;
+  bool vok[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) vok[v] = (32 * v + lane) * V < B;
 
   float lg[BPL];
 #pragma unroll
   for (int b = 0; b < BPL; ++b) lg[b] = 0.f;
-
-  Vec<BPL> ring[PF];
-  int id_cur = lane < K ? ids[lane] : 0;
-  int id_nxt = 32 + lane < K ? ids[32 + lane] : 0;
-#pragma unroll
-  for (int j = 0; j < PF; ++j) {
-    const int d = __shfl_sync(FULL, id_cur, j);
-    ring[j] = (j < K && vok) ? ldrow<BPL, STREAM>(myrow + (int64_t)d * B, vhalf) : vzero<BPL>();
-  }
 
   const int nchunks = (K + 31) >> 5;
   const int nchunks_out = (kmax + 31) >> 5;
@@ -101,51 +136,119 @@ score_kernel(const __grid_constant__ ScoreParams p) {
   int bestk = 0;
 
   for (int c = 0; c < nchunks; ++c) {
+    int32_t sigp = 0;   // slack of this lane's member in slot c
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) sigp = s == c ? sig[s] : sigp;
     float pend[5];
     float pendL[5];
     float Ek = 0.f, Sk = 0.f;
 #pragma unroll
-    for (int kk = 0; kk < 32; ++kk) {
-      const int k = 32 * c + kk + 1;
-      float part = 0.f, partL = 0.f;
-      if (k <= K) {
-        // LG_k = LG_{k-1} + row d_k
-        const Vec<BPL> cur = ring[kk % PF];
+    for (int kg = 0; kg < 32; kg += G) {
+      // one group of G consecutive k = k0 .. k0+G-1 (rows j0 .. j0+G-1, one barrier)
+      const int k0 = 32 * c + kg + 1;
+      const int j0 = k0 - 1;
+      float part[G], partL[G];
 #pragma unroll
-        for (int e = 0; e < BPL; ++e) lg[e] += cur.x[e];
-        // refill the ring slot with row k + PF
-        {
-          const int jn = kk + PF;  // index within chunk c (may spill into c+1)
-          const int d = jn < 32 ? __shfl_sync(FULL, id_cur, jn & 31) : __shfl_sync(FULL, id_nxt, jn & 31);
-          const bool ok = k + PF <= K;
-          if (ok && vok) ring[kk % PF] = ldrow<BPL, STREAM>(myrow + (int64_t)d * B, vhalf);
+      for (int i = 0; i < G; ++i) part[i] = partL[i] = 0.f;
+      if (k0 <= K) {
+        mbar_wait(bar_s + 8 * ((kg / G) % 2), (uint32_t)(j0 / R) & 1u);
+        // LG_k = LG_{k-1} + row d_k, written back over row k's slot, for the G rows
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          if (k0 + i <= K) {
+            float *sl = ring + ((kg + i) % R) * SLOT + 4;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              if (vok[v]) {
+                float *pv = sl + (32 * v + lane) * V;
+                const Vec<V> x = *reinterpret_cast<const Vec<V> *>(pv);
+#pragma unroll
+                for (int e = 0; e < V; ++e) lg[v * V + e] += x.x[e];
+                st_vec<V>(pv, &lg[v * V]);
+              }
+            }
+            if (!PICK && p.EL) {
+              // E[max bin] = B - sum_{i<B} G_k(tau_i)  (summation by parts of Eq. 5)
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                  const int bin = (32 * v + lane) * V + e;  // 0-based: tau_{bin+1}
+                  if (bin < B - 1) partL[i] += ex2_approx(lg[v * V + e]);
+                }
+            }
+          }
         }
-        // stage LG_k
-        float *sg = stg[kk & 1];
-        st_stage<BPL>(sg + lane * BPL, lg);
         __syncwarp();
-        const int32_t a = p.prof.a[k - 1], wB = p.prof.wB[k - 1];
-        const uint32_t mg = p.prof.mag[k - 1], sh = p.prof.sh[k - 1];
+        // the previous group (rows j0-G .. j0-1) is fully consumed: refill it
+        // with rows j0+G .. j0+2G-1
+        if (j0 >= G) {
+          const int pg = ((kg / G) + 1) % 2;
+          const int nrows = min(max(K - (j0 + G), 0), G);
+          arm_barrier(lane == 0 && nrows > 0, bar_s + 8 * pg, (uint32_t)nrows * row_bytes);
 #pragma unroll
-        for (int s = 0; s < SLOTS; ++s) {
-          if (s < c || (s == c && lane <= kk)) {
-            const int i = lookup_bin(sig[s], a, wB, mg, sh);
-            const float pr = ex2_approx(sg[i - 1]);
-            part += pr;
-            if (!PICK && p.P) p.P[q * tri + (int64_t)k * (k - 1) / 2 + 32 * s + lane] = pr;
+          for (int i = 0; i < G; ++i) {
+            const int jn = kg + G + i;  // index of row j0+G+i within chunk c (may spill into c+1)
+            const int d = jn < 32 ? __shfl_sync(FULL, id_cur, jn & 31) : __shfl_sync(FULL, id_nxt, jn & 31);
+            const int ps = (kg + G + i) % R;
+            bulk_row<STREAM>(lane == 0 && j0 + G + i < K, ring_s + (ps * SLOT + 4) * 4, p.log2F + (int64_t)d * B,
+                             row_bytes, bar_s + 8 * pg, pol);
           }
         }
-        if (!PICK && p.EL) {
-          // E[max bin] = B - sum_{i<B} G_k(tau_i)  (summation by parts of Eq. 5)
+        int32_t a2[G], wB2[G];
+        uint32_t mg[G], sh[G];
+        uint32_t sgl[G];   // shared address of LG_{k0+i}(tau_0) = -inf; bin b at + 4b
 #pragma unroll
-          for (int e = 0; e < BPL; ++e) {
-            const int bin = lane * BPL + e;  // 0-based: tau_{bin+1}
-            if (bin < B - 1) partL += ex2_approx(lg[e]);
-          }
+        for (int i = 0; i < G; ++i) {
+          a2[i] = p.prof.a2[k0 - 1 + i];
+          wB2[i] = p.prof.wB2[k0 - 1 + i];
+          mg[i] = p.prof.mag[k0 - 1 + i];
+          sh[i] = p.prof.sh[k0 - 1 + i];
+          sgl[i] = ring_s + (((kg + i) % R) * SLOT + 3) * 4;
         }
+        // members of the full slots s < c (Duff's device on the warp-uniform c);
+        // each case scores one member against the G k's of the group (G-way ILP)
+        switch (c) {
+#define ORLOJ_FULL_SLOT(S)                                                                     \
+  case (S) + 1:                                                                                \
+    if constexpr ((S) < SLOTS) {                                                               \
+      _Pragma("unroll") for (int i = 0; i < G; ++i) {                                          \
+        const float pr = ex2_approx(lds_f32(sgl[i] + 4 * lookup_bin(sig[(S)], a2[i], wB2[i], mg[i], sh[i]))); \
+        part[i] += pr;                                                                         \
+        if (!PICK && p.P && k0 + i <= K)                                                       \
+          p.P[q * tri + (int64_t)(k0 + i) * (k0 + i - 1) / 2 + 32 * (S) + lane] = pr;          \
+      }                                                                                        \
+    }                                                                                          \
+    [[fallthrough]];
+          ORLOJ_FULL_SLOT(6)
+          ORLOJ_FULL_SLOT(5)
+          ORLOJ_FULL_SLOT(4)
+          ORLOJ_FULL_SLOT(3)
+          ORLOJ_FULL_SLOT(2)
+          ORLOJ_FULL_SLOT(1)
+          ORLOJ_FULL_SLOT(0)
+#undef ORLOJ_FULL_SLOT
+          default:
+            break;
+        }
+        // the partial slot c: member 32c + lane joins at k = 32c + lane + 1
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          float pr = ex2_approx(lds_f32(sgl[i] + 4 * lookup_bin(sigp, a2[i], wB2[i], mg[i], sh[i])));
+          pr = lane <= kg + i ? pr : 0.f;
+          part[i] += pr;
+          if (!PICK && p.P && lane <= kg + i && k0 + i <= K)
+            p.P[q * tri + (int64_t)(k0 + i) * (k0 + i - 1) / 2 + 32 * c + lane] = pr;
+        }
+#pragma unroll
+        for (int i = 0; i < G; ++i)
+          if (k0 + i > K) part[i] = partL[i] = 0.f;   // tail of the last group
       }
-      Ek = bfly_push(pend, part, kk, lane);
-      if (!PICK && p.EL) Sk = bfly_push(pendL, partL, kk, lane);
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        Ek = bfly_push(pend, part[i], kg + i, lane);
+        if (!PICK && p.EL) Sk = bfly_push(pendL, partL[i], kg + i, lane);
+      }
     }
     // lane l now holds E_k for k = 32c + l + 1
     const int k = 32 * c + lane + 1;

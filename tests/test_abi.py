@@ -51,7 +51,8 @@ def test_sync_argument_errors(lib):
     w2 = np.array([1 << 30], np.int64)
     prof2 = _abi.LatencyProfile(1, a.ctypes.data, w2.ctypes.data)
     assert lib.orloj_pick_batch(ctypes.byref(st), ctypes.byref(prof2), ctypes.byref(q), bk, bk, None) == 4
-    assert lib.orloj_score_batches(ctypes.byref(st), ctypes.byref(prof), ctypes.byref(q), None, None, None,
+    q1 = _abi.QueuesC(1, 16, None, 16, 16, 16)
+    assert lib.orloj_score_batches(ctypes.byref(st), ctypes.byref(prof), ctypes.byref(q1), None, None, None,
                                    None) == 1
     assert lib.orloj_pick_batch_host_workspace(10, 100) > 0
 
