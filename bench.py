@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: only the timed pick loop")
+    ap.add_argument("--only-replay", action="store_true", help="profiling mode: only the replay sweep")
     return ap.parse_args()
 
 
@@ -223,6 +224,12 @@ def main():
         tt = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
+
+    if args.only_replay:
+        r = run_replay(args, rank, world, dev, barrier, max_over_ranks)
+        if rank == 0:
+            print(json.dumps({"replay": r}), flush=True)
+        return
 
     # ---------------- C3 pick: setup (untimed) ----------------
     cfg = gen.config3(Q=args.queues, kmax=args.kmax, instance=rank)
