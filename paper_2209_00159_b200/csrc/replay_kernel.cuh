@@ -3,16 +3,20 @@
 //
 // Scenario state is (t, cursor, carry): with a constant SLO per scenario the
 // deadline order equals arrival order (A9), so the live queue is exactly the
-// window remainder ("carry", <= kmax entries, kept in shared memory) followed by
-// arrivals [cursor, ...) with arrival <= t.  Per decision:
+// window remainder ("carry", <= kmax entries) followed by arrivals [cursor, ...)
+// with arrival <= t.  The window lives in shared memory as member fields
+// (deadline, distribution, hidden true bin), so carried members are never
+// re-read from HBM, and each lane holds one of the next 32 arrivals in
+// registers (refilled one decision ahead), so admissions do not wait on HBM.
+// Per decision:
 //   1. scan: carry, then admitted arrivals, 32 at a time; ballots split
 //      hopeless (P_r(1) = 0 exactly <=> i*(r,1) < first non-empty bin of d_r,
 //      integer test) from kept members; kept ones are compacted into the window
-//      with popc ranks (shared-memory scatter), stopping at kmax (A16);
+//      by popc rank, stopping at kmax (A16);
 //   2. score the window exactly like score_kernel (lane = member, lanes also
-//      own the bins; store rows from shared memory), keeping the 32 per-lane
-//      P_lane(k) in registers and reducing them with the transposing butterfly
-//      (pairs beyond the window skipped);
+//      own the bins; store rows from shared memory; 4 k per staging pass for
+//      4-way ILP); P_r(k) goes to a per-warp [k][r] shared matrix and lane k-1
+//      sums row k with 128-bit loads (conflict-free, stride 36);
 //   3. argmax (REDUX max on float bits, then min k), dispatch: dur = a_k* +
 //      w_k* * max true_bin (REDUX max), finished / late by ballot (A11, A17);
 //   4. t += dur; carry = window[k*:].
@@ -40,22 +44,39 @@ struct ReplayParams {
 
 constexpr int REPLAY_WARPS = 4;
 
+// Per-warp shared memory: four staging rows, the window's member fields and
+// the P[k][r] matrix (row stride 36 floats: conflict-free 128-bit row reads).
 template <int BPL>
-__global__ void __launch_bounds__(REPLAY_WARPS * 32)
+struct ReplayWarpSmem {
+  static constexpr int STG = 32 * BPL + 4;
+  static constexpr int PSTRIDE = 36;
+  static constexpr size_t BYTES = (size_t)(4 * STG) * 4 + 32 * (8 + 4 + 4) + 32 * PSTRIDE * 4;
+  __host__ __device__ static constexpr size_t bytes() { return BYTES; }
+};
+
+#ifndef ORLOJ_REPLAY_MIN_BLOCKS
+#define ORLOJ_REPLAY_MIN_BLOCKS 8
+#endif
+
+template <int BPL>
+__global__ void __launch_bounds__(REPLAY_WARPS * 32, ORLOJ_REPLAY_MIN_BLOCKS)
 replay_kernel(const __grid_constant__ ReplayParams p) {
-  constexpr int BPAD = 32 * BPL;
-  constexpr int STG = BPAD + 4;
+  constexpr int STG = ReplayWarpSmem<BPL>::STG;
+  constexpr int PST = ReplayWarpSmem<BPL>::PSTRIDE;
 
   extern __shared__ __align__(16) float s_dyn[];
   const int D = p.D, B = p.B;
-  float *s_store = s_dyn;                                       // [D][B]
+  float *s_store = s_dyn;                                                  // [D][B]
   int32_t *s_mmin = reinterpret_cast<int32_t *>(s_store + (size_t)D * B);  // [D]
-  float *s_warp = reinterpret_cast<float *>(s_mmin + ((D + 3) & ~3));
+  char *s_warp = reinterpret_cast<char *>(s_mmin + ((D + 3) & ~3));
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  float *stg0 = s_warp + wid * (2 * STG + 32) + 4;
-  float *stg1 = stg0 + STG;
-  int32_t *s_win = reinterpret_cast<int32_t *>(stg1 + BPAD);    // [32] window (scenario-relative indices)
+  char *my = s_warp + wid * ReplayWarpSmem<BPL>::bytes();
+  float *stg = reinterpret_cast<float *>(my) + 4;                  // 4 staging rows, stride STG
+  int64_t *w_dl = reinterpret_cast<int64_t *>(my + 4 * STG * 4);  // window deadlines
+  int32_t *w_d = reinterpret_cast<int32_t *>(w_dl + 32);          // window distributions
+  int32_t *w_tb = w_d + 32;                                        // window true bins
+  float *Pm = reinterpret_cast<float *>(w_tb + 32);                // P[k-1][r], stride PST
 
   // stage the (small) store and the first non-empty bin of every distribution
   for (int e = threadIdx.x; e < D * B; e += blockDim.x) s_store[e] = p.log2F[e];
@@ -66,10 +87,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       if (s_store[d * B + i] != -INFINITY) m = i + 1;
     s_mmin[d] = m;
   }
-  if (lane == 0) {
-    stg0[-1] = -INFINITY;
-    stg1[-1] = -INFINITY;
-  }
+  if (lane < 4) stg[lane * STG - 1] = -INFINITY;
   __syncthreads();
 
   const int64_t s = (int64_t)blockIdx.x * REPLAY_WARPS + wid;
@@ -87,45 +105,50 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
 
   int64_t t = INT64_MIN;
   int64_t cursor = 0;
+  // lookahead: lane l holds arrivals[cursor + l] (INT64_MAX beyond the trace)
+  int64_t ua = lane < n ? arr[lane] : INT64_MAX;
+  int ud = lane < n ? dis[lane] : 0;
+  int ut = lane < n ? (int)tbs[lane] : 0;
   int ncarry = 0, carry_off = 0;
   long long c_fin = 0, c_drop = 0, c_late = 0, c_bat = 0, c_busy = 0;
   int64_t ndec = 0;
 
   while (cursor < n || ncarry > 0) {
-    if (ncarry == 0) {
-      const int64_t ac = arr[cursor];
-      if (ac > t) t = ac;
-    }
+    const int64_t next_arr = __shfl_sync(FULL, ua, 0);
+    if (ncarry == 0 && next_arr > t) t = next_arr;  // idle worker: jump to the next arrival (A15)
     // ---- 1. scan -------------------------------------------------------
     int wc = 0;
     if (ncarry > 0) {
       const bool valid = lane < ncarry;
-      const int r = valid ? s_win[carry_off + lane] : 0;
+      int64_t Dr = 0;
+      int dr = 0, tr = 0;
       bool keep = false;
       if (valid) {
-        const int32_t i1 = lookup_bin(sigma2(arr[r] + slo - t), a21, wB21, mg1, sh1);
-        keep = i1 >= s_mmin[dis[r]];
+        Dr = w_dl[carry_off + lane];
+        dr = w_d[carry_off + lane];
+        tr = w_tb[carry_off + lane];
+        keep = lookup_bin(sigma2(Dr - t), a21, wB21, mg1, sh1) >= s_mmin[dr];
       }
       const unsigned vm = __ballot_sync(FULL, valid);
       const unsigned km = __ballot_sync(FULL, keep);
       c_drop += __popc(vm & ~km);
       __syncwarp();
-      if (keep) s_win[__popc(km & ((1u << lane) - 1u))] = r;
+      if (keep) {
+        const int slot = __popc(km & ((1u << lane) - 1u));
+        w_dl[slot] = Dr;
+        w_d[slot] = dr;
+        w_tb[slot] = tr;
+      }
       wc = __popc(km);
     }
-    while (wc < kmax && cursor < n) {
-      const int64_t idx = cursor + lane;
-      const bool valid = idx < n && arr[idx] <= t;
+    while (wc < kmax) {
+      const bool valid = ua <= t;  // arrivals are sorted: valid lanes form a prefix
       const unsigned vm = __ballot_sync(FULL, valid);
       if (vm == 0) break;
-      bool keep = false;
-      if (valid) {
-        const int32_t i1 = lookup_bin(sigma2(arr[idx] + slo - t), a21, wB21, mg1, sh1);
-        keep = i1 >= s_mmin[dis[idx]];
-      }
+      const bool keep = valid && lookup_bin(sigma2(ua + slo - t), a21, wB21, mg1, sh1) >= s_mmin[ud];
       const unsigned km = __ballot_sync(FULL, keep);
       const int need = kmax - wc;
-      unsigned consumed = vm;  // arrivals are sorted: vm is a prefix
+      unsigned consumed = vm;
       if (__popc(km) >= need) {
         // lane of the need-th kept member: its inclusive kept-rank equals need
         const unsigned le = (lane == 31) ? FULL : ((1u << (lane + 1)) - 1u);
@@ -135,10 +158,30 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       }
       const unsigned kc = km & consumed;
       c_drop += __popc(vm & consumed & ~km);
-      if ((kc >> lane) & 1u) s_win[wc + __popc(kc & ((1u << lane) - 1u))] = (int)idx;
+      if ((kc >> lane) & 1u) {
+        const int slot = wc + __popc(kc & ((1u << lane) - 1u));
+        w_dl[slot] = ua + slo;
+        w_d[slot] = ud;
+        w_tb[slot] = ut;
+      }
       wc += __popc(kc);
       const int nc = __popc(consumed);
       cursor += nc;
+      // shift the lookahead by nc lanes; refill its tail from HBM (used next decision)
+      const int src = (lane + nc) & 31;
+      const int64_t sa = __shfl_sync(FULL, ua, src);
+      const int sd = __shfl_sync(FULL, ud, src);
+      const int st = __shfl_sync(FULL, ut, src);
+      if (lane + nc < 32) {
+        ua = sa;
+        ud = sd;
+        ut = st;
+      } else {
+        const int64_t idx = cursor + lane;
+        ua = idx < n ? arr[idx] : INT64_MAX;
+        ud = idx < n ? dis[idx] : 0;
+        ut = idx < n ? (int)tbs[idx] : 0;
+      }
       if (nc < 32) break;
     }
     ncarry = 0;
@@ -149,47 +192,52 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
 
     // ---- 2. score the window ---------------------------------------------
     const bool mem = lane < wc;
-    const int r = mem ? s_win[lane] : 0;
-    const int64_t Dr = mem ? arr[r] + slo : 0;
+    const int64_t Dr = mem ? w_dl[lane] : 0;
     const int32_t sig = mem ? sigma2(Dr - t) : 0;
-    const int dr = mem ? dis[r] : 0;
-    const int tb = mem ? (int)tbs[r] : 0;
+    const int dr = mem ? w_d[lane] : 0;
+    const int tb = mem ? w_tb[lane] : 0;
 
     float lg[BPL];
 #pragma unroll
     for (int b = 0; b < BPL; ++b) lg[b] = 0.f;
     const bool vok = lane * BPL < B;
-    float v[32];
 #pragma unroll
-    for (int kk = 0; kk < 32; ++kk) {
-      v[kk] = 0.f;
-      if (kk < wc) {
-        const int d = __shfl_sync(FULL, dr, kk);
-        if (vok) {
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      if (k0 >= wc) break;
+      __syncwarp();  // the previous group's gathers are done before its staging rows are rewritten
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int d = __shfl_sync(FULL, dr, k0 + i);  // beyond wc: lane >= wc holds id 0 (harmless)
+        if (vok && k0 + i < wc) {
           const Vec<BPL> x = *reinterpret_cast<const Vec<BPL> *>(s_store + d * B + lane * BPL);
 #pragma unroll
           for (int e = 0; e < BPL; ++e) lg[e] += x.x[e];
         }
-        float *sg = (kk & 1) ? stg1 : stg0;
-        st_vec<BPL>(sg + lane * BPL, lg);
-        __syncwarp();
-        if (lane <= kk) {
-          const int i = lookup_bin(sig, p.prof.a2[kk], p.prof.wB2[kk], p.prof.mag[kk], p.prof.sh[kk]);
-          v[kk] = ex2_approx(sg[i - 1]);
-        }
+        st_vec<BPL>(stg + i * STG + lane * BPL, lg);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int kk = k0 + i;  // k - 1
+        const int bi = lookup_bin(sig, p.prof.a2[kk], p.prof.wB2[kk], p.prof.mag[kk], p.prof.sh[kk]);
+        const float pr = ex2_approx(stg[i * STG + bi - 1]);
+        Pm[kk * PST + lane] = lane <= kk ? pr : 0.f;
       }
     }
-    // transposing butterfly; pairs entirely beyond the window are zero
-#pragma unroll
-    for (int L = 0; L < 5; ++L) {
-#pragma unroll
-      for (int m = 0; m < (16 >> L); ++m) {
-        if ((m << (L + 1)) < wc) v[m] = bfly_combine(v[2 * m], v[2 * m + 1], L, lane);
-        else v[m] = 0.f;
+    __syncwarp();
+    // E_k = sum_r P[k-1][r] in lane k-1 (rows at or beyond wc are never read)
+    float E = 0.f;
+    if (mem) {
+      const float4 *row = reinterpret_cast<const float4 *>(Pm + lane * PST);
+      for (int j = 0; 4 * j <= lane; ++j) {
+        const float4 x = row[j];
+        E += x.x;
+        E += x.y;
+        E += x.z;
+        E += x.w;
       }
     }
     // ---- 3. argmax + dispatch ----------------------------------------------
-    const float E = mem ? v[0] : 0.f;
     const uint32_t mx = __reduce_max_sync(FULL, mem ? __float_as_uint(E) : 0u);
     const int kstar = (int)__reduce_min_sync(FULL, (mem && __float_as_uint(E) == mx) ? (uint32_t)lane : 32u) + 1;
     const int mbin = (int)__reduce_max_sync(FULL, lane < kstar ? (uint32_t)tb : 0u);

@@ -55,7 +55,7 @@ struct ScoreShape {
   static constexpr int R = ORLOJ_RING;         // ring slots per warp (two groups of G rows)
   static constexpr int G = R / 2;              // rows per barrier group; divides 32
   static constexpr int SLOT = 32 * BPL + 4;    // floats per slot incl. the 16-B head
-  static constexpr size_t smem_bytes() { return (size_t)SCORE_WARPS * (R * SLOT * 4 + 2 * 8); }
+  __host__ __device__ static constexpr size_t smem_bytes() { return (size_t)SCORE_WARPS * (R * SLOT * 4 + 2 * 8); }
 };
 
 template <int BPL, int SLOTS, bool PICK, bool STREAM>
