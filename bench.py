@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--replay-arrivals", type=int, default=100_000)
     ap.add_argument("--replay-reps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 workload lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: only the timed pick loop")
@@ -295,7 +297,7 @@ def main():
         pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()  # noqa: E731
         h_off, h_dl = pin(qn.offsets, np.int64), pin(qn.deadline, np.int64)
         h_dist, h_now = pin(qn.dist, np.int32), pin(qn.now, np.int64)
-        hp = orj.HostPicker(store, prof, Q, qn.N, dev)
+        hp = orj.HostPicker(store, prof, qn.offsets, chunks=args.e2e_chunks, streams=2, device=dev)
         for _ in range(max(1, args.warmup)):
             hp.pick(h_off, h_dl, h_dist, h_now, stream)
         torch.cuda.synchronize()
@@ -313,7 +315,8 @@ def main():
         result["e2e"] = {"value": world * Q / (e_ms / 1e3), "unit": "decisions/s",
                          "h2d_bytes_per_step": hp.h2d_bytes(), "d2h_bytes_per_step": hp.d2h_bytes(),
                          "ms_per_step": e_ms, "steps": e_steps,
-                         "path": "orloj_pick_batch_host: pinned host queues -> H2D -> kernel -> D2H, one stream"}
+                         "path": f"orloj_pick_batch_host: pinned host queues -> H2D -> kernel -> D2H, "
+                                 f"{args.e2e_chunks} chunks pipelined on 2 streams"}
         del hp
 
     # ---------------- cpu baseline (rank 0, N = 1 only) ----------------
@@ -328,6 +331,10 @@ def main():
     del store, qs
     torch.cuda.empty_cache()
 
+    # ---------------- other workload shapes (C2 SkipNet-like, C4 static CNN) ----------------
+    if not args.no_extra:
+        result["workloads"] = run_other_workloads(args, dev, max_over_ranks, world)
+
     # ---------------- replay sweep (C5) ----------------
     if not args.no_replay:
         result["replay"] = run_replay(args, rank, world, dev, barrier, max_over_ranks)
@@ -336,6 +343,59 @@ def main():
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_other_workloads(args, dev, max_over_ranks, world):
+    """Decisions/s on the other §8(d) score shapes (same kernel family):
+    C2 (1,024 SkipNet-like queues x 64, kmax 32, B 64): 100 back-to-back picks
+    captured in one CUDA graph; C4 (1,048,576 static-CNN queues x 32, point
+    masses, B 32): one pick per step."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+
+    out = {}
+    stream = torch.cuda.Stream(dev)
+    for name, cfg, reps in (("C2", gen.config2(), 100), ("C4", gen.config4(), 1)):
+        store = wl.score_store(cfg, dev)
+        prof = wl.profile(cfg.profile)
+        qs = wl.device_queues(cfg.queues, dev, with_arrival=False)
+        Q = cfg.queues.Q
+        cands = int(np.minimum(np.diff(cfg.queues.offsets), cfg.kmax).sum())
+        bk = torch.empty(Q, dtype=torch.int32, device=dev)
+        bE = torch.empty(Q, dtype=torch.float32, device=dev)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                orj.pick_batch(store, prof, qs, bk, bE, stream)
+        torch.cuda.synchronize()
+        if reps > 1:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(reps):
+                    orj.pick_batch(store, prof, qs, bk, bE, stream)
+            run = g.replay
+        else:
+            def run():
+                orj.pick_batch(store, prof, qs, bk, bE, stream)
+        with torch.cuda.stream(stream):
+            run()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            iters = 20
+            e0.record(stream)
+            for _ in range(iters):
+                run()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1)) / (iters * reps)
+        out[name] = {"workload": cfg.name, "queues": Q, "kmax": cfg.kmax, "bins": cfg.fam.B,
+                     "us_per_pick": 1e3 * ms, "decisions_per_s": world * Q / (ms / 1e3),
+                     "candidates_per_s": world * cands / (ms / 1e3),
+                     "timing": f"{iters} x " + (f"CUDA graph of {reps} picks" if reps > 1 else "1 pick")}
+        del store, qs
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_replay(args, rank, world, dev, barrier, max_over_ranks):

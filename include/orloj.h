@@ -116,7 +116,9 @@ typedef struct {
  * ------------------------------------------------------------------------- */
 typedef struct {
   int64_t num_queues;            /* Q >= 0 */
-  const int64_t *queue_offsets;  /* device [Q+1], CSR: queue q = members [off[q], off[q+1]) */
+  const int64_t *queue_offsets;  /* device [Q+1], CSR: queue q = members [off[q]-off[0], off[q+1]-off[0])
+                                    of the member arrays (off[0] may be any base, e.g. a chunk of a
+                                    larger queue set) */
   const int64_t *arrival_ticks;  /* device [N] release times, or NULL; read only by validation (tie order) */
   const int64_t *deadline_ticks; /* device [N]; per queue ordered by (deadline, arrival, index) (A9) */
   const int32_t *dist_id;        /* device [N], 0 <= dist_id < store.num_dists */
@@ -149,7 +151,9 @@ orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_prof
  * memory: enqueues H2D copies of the queue arrays into `workspace`, the pick
  * kernel and D2H copies of the results, all on `stream`; the caller
  * synchronises.  Host arrays must stay valid until the stream reaches the
- * copies.  workspace: device, >= orloj_pick_batch_host_workspace(Q, N) bytes,
+ * copies.  queue_offsets_host follows the orloj_queues convention (any base),
+ * so a caller can pipeline chunks of one queue set on several streams, each
+ * with its own workspace, to overlap copies with compute.  workspace: device, >= orloj_pick_batch_host_workspace(Q, N) bytes,
  * 256-byte aligned. */
 size_t orloj_pick_batch_host_workspace(int64_t num_queues, int64_t num_members);
 orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency_profile *profile,

@@ -205,23 +205,36 @@ def pick_batch(store: HistogramStore, profile: LatencyProfile, queues: Queues, b
 
 
 class HostPicker:
-    """End-to-end pick for queues in pinned host memory (orloj_pick_batch_host):
-    H2D copies, kernel and D2H copies enqueued by the library on one stream."""
+    """End-to-end pick for queues in pinned host memory (orloj_pick_batch_host).
 
-    def __init__(self, store: HistogramStore, profile: LatencyProfile, num_queues: int, num_members: int,
-                 device="cuda"):
+    The queue set is cut into `chunks` contiguous chunks issued round-robin on
+    `streams` CUDA streams, each with its own device workspace: every call
+    enqueues its chunk's H2D copies, the pick kernel and the D2H copies of the
+    results, so the copy of chunk c+1 overlaps the kernel of chunk c (the copy
+    engine and the SMs run concurrently).  `pick` returns after enqueueing and
+    making the caller's stream wait for every chunk."""
+
+    def __init__(self, store: HistogramStore, profile: LatencyProfile, offsets, chunks: int = 1,
+                 streams: int = 1, device="cuda"):
         self.store, self.profile = store, profile
-        self.Q, self.N = int(num_queues), int(num_members)
-        nbytes = _abi.lib().orloj_pick_batch_host_workspace(self.Q, self.N)
-        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
-        base = self.workspace.data_ptr()
-        self._ws = (base + 255) & ~255
-        self._ws_bytes = nbytes
+        off = np.asarray(offsets, dtype=np.int64)
+        self.Q, self.N = len(off) - 1, int(off[-1] - off[0])
+        chunks = max(1, min(int(chunks), max(self.Q, 1)))
+        qb = np.linspace(0, self.Q, chunks + 1).astype(np.int64)
+        self.bounds = [(int(a), int(b), int(off[a] - off[0]), int(off[b] - off[0])) for a, b in zip(qb[:-1], qb[1:])]
+        self.streams = [torch.cuda.Stream(device) for _ in range(max(1, int(streams)))]
+        self.ws = []
+        for i in range(len(self.streams)):
+            need = max(_abi.lib().orloj_pick_batch_host_workspace(b - a, m1 - m0)
+                       for j, (a, b, m0, m1) in enumerate(self.bounds) if j % len(self.streams) == i) \
+                if len(self.bounds) > i else 256
+            buf = torch.empty(need + 256, dtype=torch.uint8, device=device)
+            self.ws.append((buf, (buf.data_ptr() + 255) & ~255, need))
         self.best_k = torch.empty(self.Q, dtype=torch.int32).pin_memory()
         self.best_E = torch.empty(self.Q, dtype=torch.float32).pin_memory()
 
     def h2d_bytes(self):
-        return (self.Q + 1) * 8 + self.N * 8 + self.N * 4 + self.Q * 8
+        return sum((b - a + 1) * 8 + (m1 - m0) * 12 + (b - a) * 8 for a, b, m0, m1 in self.bounds)
 
     def d2h_bytes(self):
         return self.Q * 8
@@ -232,10 +245,23 @@ class HostPicker:
                          (dist, torch.int32, "dist"), (now, torch.int64, "now")):
             if t.is_cuda or t.dtype != dt or not t.is_contiguous():
                 raise OrlojError(1, f"{n} must be a contiguous host {dt} tensor (pinned for async copies)")
-        _abi.check(_abi.lib().orloj_pick_batch_host(
-            self.store.c(), self.profile.c(), self.Q, offsets.data_ptr(), deadline.data_ptr(), dist.data_ptr(),
-            now.data_ptr(), self.best_k.data_ptr(), self.best_E.data_ptr(), self._ws, self._ws_bytes,
-            _stream_ptr(stream)))
+        main = stream or torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(main)
+        for s in self.streams:
+            s.wait_event(start)
+        L = _abi.lib()
+        for j, (a, b, m0, m1) in enumerate(self.bounds):
+            s = self.streams[j % len(self.streams)]
+            _, ws, wsb = self.ws[j % len(self.streams)]
+            _abi.check(L.orloj_pick_batch_host(
+                self.store.c(), self.profile.c(), b - a, offsets.data_ptr() + 8 * a, deadline.data_ptr() + 8 * m0,
+                dist.data_ptr() + 4 * m0, now.data_ptr() + 8 * a, self.best_k.data_ptr() + 4 * a,
+                self.best_E.data_ptr() + 4 * a, ws, wsb, s.cuda_stream))
+        for s in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            main.wait_event(ev)
         return self.best_k, self.best_E
 
 

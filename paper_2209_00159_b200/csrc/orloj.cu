@@ -105,51 +105,63 @@ int slots_for(int kmax) {
   return c <= 1 ? 1 : c <= 2 ? 2 : c <= 4 ? 4 : 8;
 }
 
-template <int BPL, int SLOTS, bool PICK, bool STREAM>
+// Row source of the score kernel: TMA ring from HBM (STREAM adds L1 bypass and
+// L2 evict-first for stores larger than L2), or the whole store staged in
+// shared memory when it is small (a few application histograms).
+enum class RowSrc { Tma, TmaStream, Smem };
+constexpr int64_t STREAM_STORE_BYTES = 256ll << 20;
+constexpr int64_t SMEM_STORE_BYTES = 48ll << 10;
+
+template <int BPL, int SLOTS, bool PICK, bool STREAM, bool SMEMS>
 cudaError_t launch_score_t(const ScoreParams &p, cudaStream_t s) {
   const int64_t blocks = (p.Q + SCORE_WARPS - 1) / SCORE_WARPS;
-  const size_t smem = ScoreShape<BPL>::smem_bytes();
+  const size_t base = ScoreShape<BPL>::smem_bytes();
+  const size_t smem = base + (SMEMS ? (size_t)p.D * p.B * 4 : 0);
+  const size_t cap = base + (SMEMS ? (size_t)SMEM_STORE_BYTES : 0);
   static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
   if (!configured.load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<BPL, SLOTS, PICK, STREAM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
     if (e != cudaSuccess) return e;
     configured.store(true, std::memory_order_release);
   }
-  score_kernel<BPL, SLOTS, PICK, STREAM><<<(unsigned)blocks, SCORE_WARPS * 32, smem, s>>>(p);
+  score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS><<<(unsigned)blocks, SCORE_WARPS * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
-template <int BPL, bool PICK, bool STREAM>
-cudaError_t launch_score_s(const ScoreParams &p, int slots, cudaStream_t s) {
-  switch (slots) {
-    case 1: return launch_score_t<BPL, 1, PICK, STREAM>(p, s);
-    case 2: return launch_score_t<BPL, 2, PICK, STREAM>(p, s);
-    case 4: return launch_score_t<BPL, 4, PICK, STREAM>(p, s);
-    default: return launch_score_t<BPL, 8, PICK, STREAM>(p, s);
+template <int BPL, bool PICK, bool STREAM, bool SMEMS>
+cudaError_t launch_score_s(const ScoreParams &p, cudaStream_t s) {
+  switch (slots_for(p.kmax)) {
+    case 1: return launch_score_t<BPL, 1, PICK, STREAM, SMEMS>(p, s);
+    case 2: return launch_score_t<BPL, 2, PICK, STREAM, SMEMS>(p, s);
+    case 4: return launch_score_t<BPL, 4, PICK, STREAM, SMEMS>(p, s);
+    default: return launch_score_t<BPL, 8, PICK, STREAM, SMEMS>(p, s);
   }
+}
+
+template <int BPL, bool PICK>
+cudaError_t launch_score_r(const ScoreParams &p, RowSrc src, cudaStream_t s) {
+  if (src == RowSrc::Smem) return launch_score_s<BPL, PICK, false, true>(p, s);
+  if constexpr (BPL == 8)
+    if (src == RowSrc::TmaStream) return launch_score_s<8, PICK, true, false>(p, s);
+  return launch_score_s<BPL, PICK, false, false>(p, s);
 }
 
 template <bool PICK>
-cudaError_t launch_score_b(const ScoreParams &p, bool stream, cudaStream_t s) {
-  const int slots = slots_for(p.kmax);
+cudaError_t launch_score_b(const ScoreParams &p, RowSrc src, cudaStream_t s) {
   switch (bins_per_lane(p.B)) {
-    case 1: return launch_score_s<1, PICK, false>(p, slots, s);
-    case 2: return launch_score_s<2, PICK, false>(p, slots, s);
-    case 4: return launch_score_s<4, PICK, false>(p, slots, s);
-    default:
-      return stream ? launch_score_s<8, PICK, true>(p, slots, s) : launch_score_s<8, PICK, false>(p, slots, s);
+    case 1: return launch_score_r<1, PICK>(p, src, s);
+    case 2: return launch_score_r<2, PICK>(p, src, s);
+    case 4: return launch_score_r<4, PICK>(p, src, s);
+    default: return launch_score_r<8, PICK>(p, src, s);
   }
 }
 
-// Rows streamed once (the per-request store of C3, larger than L2) bypass L1
-// and are evict-first in L2; small shared stores (a few applications) stay
-// cacheable.
-constexpr int64_t STREAM_STORE_BYTES = 256ll << 20;
-
 cudaError_t launch_score(const ScoreParams &p, bool pick, int64_t store_bytes, cudaStream_t s) {
-  const bool stream = store_bytes > STREAM_STORE_BYTES;
-  return pick ? launch_score_b<true>(p, stream, s) : launch_score_b<false>(p, stream, s);
+  const RowSrc src = store_bytes <= SMEM_STORE_BYTES ? RowSrc::Smem
+                     : store_bytes > STREAM_STORE_BYTES ? RowSrc::TmaStream
+                                                        : RowSrc::Tma;
+  return pick ? launch_score_b<true>(p, src, s) : launch_score_b<false>(p, src, s);
 }
 
 orloj_status prepare_score(const orloj_store *store, const orloj_latency_profile *profile,
@@ -160,6 +172,7 @@ orloj_status prepare_score(const orloj_store *store, const orloj_latency_profile
   std::memset(p, 0, sizeof(*p));
   if ((st = compile_profile(profile, store->num_bins, ORLOJ_MAX_KMAX, &p->prof))) return st;
   p->log2F = store->log2_cdf;
+  p->D = store->num_dists;
   p->B = store->num_bins;
   p->kmax = profile->kmax;
   p->Q = queues->num_queues;
@@ -258,7 +271,7 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
                                    void *stream) {
   if (Q < 0 || !off_h || (Q > 0 && (!now_h || !bk_h || !bE_h)))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: bad host arrays");
-  const int64_t N = off_h[Q];
+  const int64_t N = off_h[Q] - off_h[0];
   if (N < 0 || (N > 0 && (!dl_h || !dist_h)))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: bad member arrays");
   if (!ws || ((uintptr_t)ws & 255u) || ws_bytes < orloj_pick_batch_host_workspace(Q, N))

@@ -29,6 +29,7 @@ namespace orloj {
 
 struct ScoreParams {
   const float *log2F;
+  int32_t D;
   int32_t B;
   int32_t kmax;
   int64_t Q;
@@ -58,7 +59,10 @@ struct ScoreShape {
   __host__ __device__ static constexpr size_t smem_bytes() { return (size_t)SCORE_WARPS * (R * SLOT * 4 + 2 * 8); }
 };
 
-template <int BPL, int SLOTS, bool PICK, bool STREAM>
+// SMEMS: the whole store (a few application histograms, D*B*4 <= 48 KiB) is
+// staged in shared memory once per CTA and rows are read from there; the TMA
+// ring is then unused and its slots only stage LG_k.
+template <int BPL, int SLOTS, bool PICK, bool STREAM, bool SMEMS>
 __global__ void __launch_bounds__(SCORE_WARPS * 32)
 score_kernel(const __grid_constant__ ScoreParams p) {
   constexpr int V = BPL < 4 ? BPL : 4;      // floats per vector
@@ -72,14 +76,21 @@ score_kernel(const __grid_constant__ ScoreParams p) {
   const int wid = threadIdx.x >> 5;
   float *ring = s_dyn + wid * (R * SLOT);                       // slot j: ring + j*SLOT, row at +4
   uint64_t *bars = reinterpret_cast<uint64_t *>(s_dyn + SCORE_WARPS * R * SLOT) + wid * 2;
+  float *s_store = reinterpret_cast<float *>(s_dyn + SCORE_WARPS * R * SLOT + 2 * 2 * SCORE_WARPS);
+  if constexpr (SMEMS) {
+    const int DB = p.D * p.B;
+    for (int e = threadIdx.x * 4; e < DB; e += blockDim.x * 4)
+      *reinterpret_cast<float4 *>(s_store + e) = __ldg(reinterpret_cast<const float4 *>(p.log2F + e));
+    __syncthreads();
+  }
 
   const int64_t q = (int64_t)blockIdx.x * SCORE_WARPS + wid;
   if (q >= p.Q) return;
 
   const int B = p.B;
   const int kmax = p.kmax;
-  const int64_t off = p.offsets[q];
-  const int64_t n = p.offsets[q + 1] - off;
+  const int64_t off = p.offsets[q] - p.offsets[0];   // offsets may start at any base (chunked calls)
+  const int64_t n = p.offsets[q + 1] - p.offsets[q];
   const int K = warp_uniform((int)(n < kmax ? n : kmax));
   const int64_t now = p.now[q];
   const int64_t *dl = p.deadline + off;
@@ -94,14 +105,16 @@ score_kernel(const __grid_constant__ ScoreParams p) {
   if (lane == 0) {
 #pragma unroll
     for (int j = 0; j < R; ++j) ring[j * SLOT + 3] = -INFINITY;
-    mbar_init(bar_s, 1);
-    mbar_init(bar_s + 8, 1);
-    mbar_init_fence();
+    if constexpr (!SMEMS) {
+      mbar_init(bar_s, 1);
+      mbar_init(bar_s + 8, 1);
+      mbar_init_fence();
+    }
   }
   __syncwarp();
   // prologue: rows 0 .. R-1 in two barrier groups
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < (SMEMS ? 0 : 2); ++g) {
     const int nrows = min(max(K - g * G, 0), G);
     arm_barrier(lane == 0 && nrows > 0, bar_s + 8 * g, (uint32_t)nrows * row_bytes);
 #pragma unroll
@@ -151,17 +164,19 @@ score_kernel(const __grid_constant__ ScoreParams p) {
 #pragma unroll
       for (int i = 0; i < G; ++i) part[i] = partL[i] = 0.f;
       if (k0 <= K) {
-        mbar_wait(bar_s + 8 * ((kg / G) % 2), (uint32_t)(j0 / R) & 1u);
-        // LG_k = LG_{k-1} + row d_k, written back over row k's slot, for the G rows
+        if constexpr (!SMEMS) mbar_wait(bar_s + 8 * ((kg / G) % 2), (uint32_t)(j0 / R) & 1u);
+        // LG_k = LG_{k-1} + row d_k, written over row k's slot, for the G rows
 #pragma unroll
         for (int i = 0; i < G; ++i) {
+          const int dsm = SMEMS ? __shfl_sync(FULL, id_cur, kg + i) : 0;   // row id (SMEMS)
           if (k0 + i <= K) {
             float *sl = ring + ((kg + i) % R) * SLOT + 4;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
               if (vok[v]) {
                 float *pv = sl + (32 * v + lane) * V;
-                const Vec<V> x = *reinterpret_cast<const Vec<V> *>(pv);
+                const Vec<V> x = *reinterpret_cast<const Vec<V> *>(
+                    SMEMS ? s_store + dsm * B + (32 * v + lane) * V : pv);
 #pragma unroll
                 for (int e = 0; e < V; ++e) lg[v * V + e] += x.x[e];
                 st_vec<V>(pv, &lg[v * V]);
@@ -182,7 +197,7 @@ score_kernel(const __grid_constant__ ScoreParams p) {
         __syncwarp();
         // the previous group (rows j0-G .. j0-1) is fully consumed: refill it
         // with rows j0+G .. j0+2G-1
-        if (j0 >= G) {
+        if (!SMEMS && j0 >= G) {
           const int pg = ((kg / G) + 1) % 2;
           const int nrows = min(max(K - (j0 + G), 0), G);
           arm_barrier(lane == 0 && nrows > 0, bar_s + 8 * pg, (uint32_t)nrows * row_bytes);

@@ -65,12 +65,11 @@ __global__ void validate_queues_kernel(const int64_t *__restrict__ off, int64_t 
                                        unsigned int *flags) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = tid; q <= Q; q += stride) {
-    if (q == 0 && off[0] != 0) atomicOr(flags, 1u);
-    if (q > 0 && off[q] < off[q - 1]) atomicOr(flags, 1u);
-  }
+  const int64_t base = off[0];
+  for (int64_t q = tid + 1; q <= Q; q += stride)
+    if (off[q] < off[q - 1]) atomicOr(flags, 1u);
   for (int64_t q = tid; q < Q; q += stride) {
-    const int64_t b = off[q], e = off[q + 1];
+    const int64_t b = off[q] - base, e = off[q + 1] - base;
     for (int64_t j = b; j < e; ++j) {
       if (dist[j] < 0 || dist[j] >= D) atomicOr(flags, 1u);
       if (j > b) {

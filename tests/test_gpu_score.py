@@ -289,12 +289,19 @@ def test_empty_and_host_path():
     assert bk0.numel() == 0
     q = c.queues
     bk, bE = orj.pick_batch(store, p, wl.device_queues(q))
-    hp = orj.HostPicker(store, p, q.Q, q.N)
     pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()  # noqa: E731
-    hk, hE = hp.pick(pin(q.offsets, np.int64), pin(q.deadline, np.int64), pin(q.dist, np.int32),
-                     pin(q.now, np.int64))
+    hargs = (pin(q.offsets, np.int64), pin(q.deadline, np.int64), pin(q.dist, np.int32), pin(q.now, np.int64))
+    for chunks, streams in ((1, 1), (5, 2), (300, 3)):
+        hp = orj.HostPicker(store, p, q.offsets, chunks=chunks, streams=streams)
+        hk, hE = hp.pick(*hargs)
+        torch.cuda.synchronize()
+        assert (hk.numpy() == bk.cpu().numpy()).all() and (hE.numpy() == bE.cpu().numpy()).all()
+    # queue offsets may start at any base (a chunk of a larger queue set)
+    sub = orj.Queues(wl.t(q.offsets[100:201], np.int64), wl.t(q.deadline[q.offsets[100]:q.offsets[200]], np.int64),
+                     wl.t(q.dist[q.offsets[100]:q.offsets[200]], np.int32), wl.t(q.now[100:200], np.int64))
+    sk, sE = orj.pick_batch(store, p, sub)
     torch.cuda.synchronize()
-    assert (hk.numpy() == bk.cpu().numpy()).all() and (hE.numpy() == bE.cpu().numpy()).all()
+    assert (sk.cpu().numpy() == bk.cpu().numpy()[100:200]).all()
 
 
 def test_store_build_values():
@@ -312,3 +319,16 @@ def test_store_build_values():
     assert ((L == -np.inf) == (F == 0)).all()
     nz = F > 0
     assert np.abs(np.exp2(L[nz]) - F[nz]).max() <= 1e-6
+
+
+@pytest.mark.parametrize("B,kmax,maxlen", [(16, 8, 12), (64, 40, 70), (100, 64, 64), (132, 130, 140)])
+def test_tma_row_path(B, kmax, maxlen):
+    """Per-request rows (store > 48 KiB, so rows come through the TMA ring
+    rather than the shared-memory store) for every bins-per-lane variant."""
+    counts, prof, q = _random_queues(7 * B + kmax, Q=97, D=9, B=B, kmax=kmax, maxlen=maxlen)
+    rng = np.random.default_rng(B)
+    D = max(9, (64 << 10) // (4 * B) + 1)
+    big = counts[rng.integers(0, counts.shape[0], D)]
+    q.dist[:] = rng.integers(0, D, len(q.dist)).astype(np.int32)
+    assert big.size * 4 > (48 << 10)
+    _check_all(big, prof, q, _run_all(big, 1, prof, q))
