@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--replay-seeds", type=int, default=256, help="seeds per (family, bucket)")
     ap.add_argument("--replay-arrivals", type=int, default=100_000)
     ap.add_argument("--replay-reps", type=int, default=2)
+    ap.add_argument("--no-shard-proxy", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 workload lines")
@@ -398,30 +399,35 @@ def run_other_workloads(args, dev, max_over_ranks, world):
     return out
 
 
-def run_replay(args, rank, world, dev, barrier, max_over_ranks):
+def build_replay(args, rank, world, dev):
+    import gen
+    import workloads as wl
+    from paper_2209_00159_b200 import parallel
+
+    nb = len(gen.BUCKET_SLO_MULTS)
+    u = np.arange(nb * args.replay_seeds)
+    mine = parallel.shard_round_robin(u // nb, rank, world)    # seed groups round-robin over ranks
+    return [wl.C5Family(name, local_ids=mine, n_arr=args.replay_arrivals, seeds_per_bucket=args.replay_seeds,
+                        device=dev) for name in gen.C5_FAMILIES]
+
+
+def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True):
+    """One sweep = the 4 family replays on 4 streams + one all-reduce of the
+    [4 x 8 x 7] int64 counters (NCCL; a no-op on one rank), all inside the
+    timed region.  Returns (ms per sweep, counters [4, 8, 7], clock summary)."""
     import torch
 
     import gen
     import paper_2209_00159_b200 as orj
-    import workloads as wl
     from paper_2209_00159_b200 import parallel
 
-    fams = []
-    for name in gen.C5_FAMILIES:
-        nb = len(gen.BUCKET_SLO_MULTS)
-        u = np.arange(nb * args.replay_seeds)
-        mine = parallel.shard_round_robin(u // nb, rank, world)    # seed groups round-robin
-        fams.append(wl.C5Family(name, local_ids=mine, n_arr=args.replay_arrivals,
-                                seeds_per_bucket=args.replay_seeds, device=dev))
-    torch.cuda.synchronize()
+    nb = len(gen.BUCKET_SLO_MULTS)
     streams = [torch.cuda.Stream(dev) for _ in fams]
     main = torch.cuda.current_stream()
-    nb = len(gen.BUCKET_SLO_MULTS)
-    tables = [torch.zeros((nb, 7), dtype=torch.int64, device=dev) for _ in fams]
+    tables = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
 
     def once():
-        for t_ in tables:
-            t_.zero_()
+        tables.zero_()
         start = torch.cuda.Event()
         start.record(main)
         for f, s, t_ in zip(fams, streams, tables):
@@ -431,6 +437,8 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
             ev = torch.cuda.Event()
             ev.record(s)
             main.wait_event(ev)
+        if reduce:
+            parallel.allreduce_counters(tables)
 
     once()  # warm-up
     torch.cuda.synchronize()
@@ -438,31 +446,46 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         e0.record(main)
-        for _ in range(args.replay_reps):
+        for _ in range(reps):
             once()
         e1.record(main)
         torch.cuda.synchronize()
     barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1)) / args.replay_reps
-    per_family = {}
-    total = torch.zeros((nb, 7), dtype=torch.int64, device=dev)
-    for f, t_ in zip(fams, tables):
-        parallel.allreduce_counters(t_)          # one NCCL all-reduce per family table
-        per_family[f.tf.fam.name] = t_.cpu().numpy()
-        total += t_
-    tot = total.cpu().numpy()
+    return max_over_ranks(e0.elapsed_time(e1)) / reps, tables.cpu().numpy(), clk.summary()
+
+
+def run_replay(args, rank, world, dev, barrier, max_over_ranks):
+    import gen
+
+    fams = build_replay(args, rank, world, dev)
+    ms, tabs, clk = time_replay(fams, args.replay_reps, dev, barrier, max_over_ranks)
+    per_family = {f.tf.fam.name: t_ for f, t_ in zip(fams, tabs)}
+    tot = tabs.sum(0)
     decisions = int(tot[:, 4].sum())
     arrivals = int(tot[:, 0].sum())
     assert (tot[:, 1] + tot[:, 2] + tot[:, 3] == tot[:, 0]).all()
     fr = {name: [round(float(x), 4) for x in (c[:, 1] / np.maximum(c[:, 0], 1))] for name, c in per_family.items()}
     util = {name: round(float(c[:, 5].sum() / max(c[:, 6].sum(), 1)), 4) for name, c in per_family.items()}
-    return {"workload": f"C5: 4 families x 8 SLO buckets x {args.replay_seeds} seeds x {args.replay_arrivals} "
-                        f"arrivals (kmax 32, B 64), scenarios round-robin over {world} ranks",
-            "value": decisions / (ms / 1e3), "unit": "decisions/s", "arrivals_per_s": arrivals / (ms / 1e3),
-            "ms_per_sweep": ms, "decisions": decisions, "arrivals": arrivals, "scaling": "strong",
-            "finish_rate_by_bucket": fr, "slo_multipliers": list(gen.BUCKET_SLO_MULTS), "utilisation": util,
-            "gpu_launches_per_sweep": len(fams), "clocks": clk.summary(),
-            "collective": "torch.distributed.all_reduce(int64 [8x7]) per family (NCCL) after the timed region"}
+    out = {"workload": f"C5: 4 families x 8 SLO buckets x {args.replay_seeds} seeds x {args.replay_arrivals} "
+                       f"arrivals (kmax 32, B 64), scenarios round-robin over {world} ranks",
+           "value": decisions / (ms / 1e3), "unit": "decisions/s", "arrivals_per_s": arrivals / (ms / 1e3),
+           "ms_per_sweep": ms, "decisions": decisions, "arrivals": arrivals, "scaling": "strong",
+           "finish_rate_by_bucket": fr, "slo_multipliers": list(gen.BUCKET_SLO_MULTS), "utilisation": util,
+           "gpu_launches_per_sweep": len(fams), "clocks": clk,
+           "collective": "one torch.distributed.all_reduce of the int64 [4 x 8 x 7] counters (NCCL) per sweep, "
+                         "inside the timed region"}
+    if world == 1 and not args.no_shard_proxy:
+        # strong-scaling proxy on one GPU: the time of rank 0's shard of an N-GPU run
+        # (everything but the ~10 us all-reduce), and the implied speed-up
+        del fams
+        proxy = {}
+        for N in (2, 4, 8):
+            sf = build_replay(args, 0, N, dev)
+            sms, _, _ = time_replay(sf, 1, dev, lambda: None, lambda x: x, reduce=False)
+            proxy[str(N)] = {"ms_rank0_shard": sms, "implied_speedup": ms / sms}
+            del sf
+        out["shard_proxy"] = proxy
+    return out
 
 
 if __name__ == "__main__":
