@@ -319,7 +319,7 @@ orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_pr
     return fail(ORLOJ_ERR_CAPACITY, "replay: store of %zu bytes exceeds the 64 KiB shared-memory budget", store_b);
   const size_t warp_b = bpl == 1 ? ReplayWarpSmem<1>::bytes() : bpl == 2 ? ReplayWarpSmem<2>::bytes()
                                                                           : ReplayWarpSmem<4>::bytes();
-  const size_t smem = store_b + (size_t)((D + 3) & ~3) * 4 + REPLAY_WARPS * warp_b;
+  const size_t smem = replay_head_bytes(D, B) + REPLAY_WARPS * warp_b;
   p.log2F = store->log2_cdf;
   p.D = D;
   p.B = B;

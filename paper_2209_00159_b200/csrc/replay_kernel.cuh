@@ -4,22 +4,23 @@
 // Scenario state is (t, cursor, carry): with a constant SLO per scenario the
 // deadline order equals arrival order (A9), so the live queue is exactly the
 // window remainder ("carry", <= kmax entries) followed by arrivals [cursor, ...)
-// with arrival <= t.  The window lives in shared memory as member fields
-// (deadline, distribution, hidden true bin), so carried members are never
-// re-read from HBM, and each lane holds one of the next 32 arrivals in
-// registers (refilled one decision ahead), so admissions do not wait on HBM.
-// Per decision:
-//   1. scan: carry, then admitted arrivals, 32 at a time; ballots split
-//      hopeless (P_r(1) = 0 exactly <=> i*(r,1) < first non-empty bin of d_r,
-//      integer test) from kept members; kept ones are compacted into the window
-//      by popc rank, stopping at kmax (A16);
-//   2. score the window exactly like score_kernel (lane = member, lanes also
-//      own the bins; store rows from shared memory; 4 k per staging pass for
-//      4-way ILP); P_r(k) goes to a per-warp [k][r] shared matrix and lane k-1
-//      sums row k with 128-bit loads (conflict-free, stride 36);
-//   3. argmax (REDUX max on float bits, then min k), dispatch: dur = a_k* +
-//      w_k* * max true_bin (REDUX max), finished / late by ballot (A11, A17);
-//   4. t += dur; carry = window[k*:].
+// with arrival <= t.  The replay is a sequential decision chain per scenario,
+// so the kernel is built for latency:
+//  * every member carries its "hopeless time" h_r = D_r - a_1 - w_1 m_min(d_r):
+//    r is hopeless at t (P_r(1) = 0 exactly, A16) iff t > h_r — one 64-bit
+//    compare (i*(r,1) >= m  <=>  sigma_r >= a_1 + w_1 m, integer-exact);
+//  * the window lives in shared memory as member fields (deadline, h,
+//    distribution, hidden true bin), each lane holds one of the next 32
+//    arrivals in registers, refilled one decision ahead and only consumed in a
+//    later decision: scanning never waits on HBM;
+//  * a window of one member is dispatched without scoring (single candidate);
+//  * scoring runs in blocks of REPLAY_KB candidate sizes (windows are short,
+//    mostly 1-3): the block's prefix rows LG_k are built and staged back to
+//    back, then every member does its lookups (REPLAY_KB-way ILP) and writes
+//    P_r(k) into a per-warp [k][r] matrix; lane k-1 then sums row k with
+//    128-bit loads and a short adder tree;
+//  * argmax by two REDUX (max of float bits, then min k), dispatch with one
+//    more REDUX (max true bin) and one ballot (finished, A11 / late, A17).
 // Counters are kept warp-uniform and added to per-bucket int64 totals at the end.
 #pragma once
 #include "common.cuh"
@@ -43,16 +44,25 @@ struct ReplayParams {
 };
 
 constexpr int REPLAY_WARPS = 4;
+#ifndef ORLOJ_REPLAY_KB
+#define ORLOJ_REPLAY_KB 2
+#endif
+constexpr int REPLAY_KB = ORLOJ_REPLAY_KB;  // candidate sizes per scoring block (windows are short: ~2-4)
 
-// Per-warp shared memory: four staging rows, the window's member fields and
-// the P[k][r] matrix (row stride 36 floats: conflict-free 128-bit row reads).
+// Per-warp shared memory: REPLAY_KB staging rows, the window's member fields
+// and the P[k][r] matrix (row stride 36 floats: conflict-free 128-bit reads).
 template <int BPL>
 struct ReplayWarpSmem {
   static constexpr int STG = 32 * BPL + 4;
   static constexpr int PSTRIDE = 36;
-  static constexpr size_t BYTES = (size_t)(4 * STG) * 4 + 32 * (8 + 4 + 4) + 32 * PSTRIDE * 4;
+  static constexpr size_t BYTES = (size_t)(REPLAY_KB * STG) * 4 + 32 * (8 + 8 + 4 + 4) + 32 * PSTRIDE * 4;
   __host__ __device__ static constexpr size_t bytes() { return BYTES; }
 };
+
+// CTA shared memory: store [D][B] floats, hopeless thresholds [D] int64 (padded), warps.
+__host__ __device__ inline size_t replay_head_bytes(int D, int B) {
+  return (size_t)D * B * 4 + (size_t)((D + 1) & ~1) * 8;
+}
 
 #ifndef ORLOJ_REPLAY_MIN_BLOCKS
 #define ORLOJ_REPLAY_MIN_BLOCKS 8
@@ -66,28 +76,29 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
 
   extern __shared__ __align__(16) float s_dyn[];
   const int D = p.D, B = p.B;
-  float *s_store = s_dyn;                                                  // [D][B]
-  int32_t *s_mmin = reinterpret_cast<int32_t *>(s_store + (size_t)D * B);  // [D]
-  char *s_warp = reinterpret_cast<char *>(s_mmin + ((D + 3) & ~3));
+  float *s_store = s_dyn;                                                   // [D][B]
+  int64_t *s_thr = reinterpret_cast<int64_t *>(s_store + (size_t)D * B);   // [D]: a_1 + w_1 m_min(d)
+  char *s_warp = reinterpret_cast<char *>(s_dyn) + replay_head_bytes(D, B);
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   char *my = s_warp + wid * ReplayWarpSmem<BPL>::bytes();
-  float *stg = reinterpret_cast<float *>(my) + 4;                  // 4 staging rows, stride STG
-  int64_t *w_dl = reinterpret_cast<int64_t *>(my + 4 * STG * 4);  // window deadlines
-  int32_t *w_d = reinterpret_cast<int32_t *>(w_dl + 32);          // window distributions
-  int32_t *w_tb = w_d + 32;                                        // window true bins
-  float *Pm = reinterpret_cast<float *>(w_tb + 32);                // P[k-1][r], stride PST
+  float *stg = reinterpret_cast<float *>(my) + 4;                            // REPLAY_KB rows, stride STG
+  int64_t *w_dl = reinterpret_cast<int64_t *>(my + REPLAY_KB * STG * 4);    // window deadlines
+  int64_t *w_h = w_dl + 32;                                                 // window hopeless times
+  int32_t *w_d = reinterpret_cast<int32_t *>(w_h + 32);                     // window distributions
+  int32_t *w_tb = w_d + 32;                                                 // window true bins
+  float *Pm = reinterpret_cast<float *>(w_tb + 32);                         // P[k-1][r], stride PST
 
-  // stage the (small) store and the first non-empty bin of every distribution
+  // stage the (small) store; hopeless threshold a_1 + w_1 m_min(d) per distribution
   for (int e = threadIdx.x; e < D * B; e += blockDim.x) s_store[e] = p.log2F[e];
   __syncthreads();
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     int m = B;
     for (int i = B - 1; i >= 0; --i)
       if (s_store[d * B + i] != -INFINITY) m = i + 1;
-    s_mmin[d] = m;
+    s_thr[d] = (int64_t)p.prof.a[0] + (int64_t)p.prof.w[0] * m;
   }
-  if (lane < 4) stg[lane * STG - 1] = -INFINITY;
+  if (lane < REPLAY_KB) stg[lane * STG - 1] = -INFINITY;
   __syncthreads();
 
   const int64_t s = (int64_t)blockIdx.x * REPLAY_WARPS + wid;
@@ -100,15 +111,17 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int64_t *arr = p.arrival + base;
   const int32_t *dis = p.dist + base;
   const int16_t *tbs = p.true_bin + base;
-  const int32_t a21 = p.prof.a2[0], wB21 = p.prof.wB2[0];
-  const uint32_t mg1 = p.prof.mag[0], sh1 = p.prof.sh[0];
 
   int64_t t = INT64_MIN;
   int64_t cursor = 0;
-  // lookahead: lane l holds arrivals[cursor + l] (INT64_MAX beyond the trace)
-  int64_t ua = lane < n ? arr[lane] : INT64_MAX;
-  int ud = lane < n ? dis[lane] : 0;
-  int ut = lane < n ? (int)tbs[lane] : 0;
+  // lookahead: lane l holds arrivals[cursor + l] (arrival INT64_MAX beyond the trace)
+  int64_t ua = INT64_MAX;
+  int ud = 0, ut = 0;
+  if (lane < n) {
+    ua = arr[lane];
+    ud = dis[lane];
+    ut = tbs[lane];
+  }
   int ncarry = 0, carry_off = 0;
   long long c_fin = 0, c_drop = 0, c_late = 0, c_bat = 0, c_busy = 0;
   int64_t ndec = 0;
@@ -120,15 +133,15 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     int wc = 0;
     if (ncarry > 0) {
       const bool valid = lane < ncarry;
-      int64_t Dr = 0;
+      int64_t Dr = 0, hr = 0;
       int dr = 0, tr = 0;
-      bool keep = false;
       if (valid) {
         Dr = w_dl[carry_off + lane];
+        hr = w_h[carry_off + lane];
         dr = w_d[carry_off + lane];
         tr = w_tb[carry_off + lane];
-        keep = lookup_bin(sigma2(Dr - t), a21, wB21, mg1, sh1) >= s_mmin[dr];
       }
+      const bool keep = valid && t <= hr;
       const unsigned vm = __ballot_sync(FULL, valid);
       const unsigned km = __ballot_sync(FULL, keep);
       c_drop += __popc(vm & ~km);
@@ -136,6 +149,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       if (keep) {
         const int slot = __popc(km & ((1u << lane) - 1u));
         w_dl[slot] = Dr;
+        w_h[slot] = hr;
         w_d[slot] = dr;
         w_tb[slot] = tr;
       }
@@ -145,7 +159,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const bool valid = ua <= t;  // arrivals are sorted: valid lanes form a prefix
       const unsigned vm = __ballot_sync(FULL, valid);
       if (vm == 0) break;
-      const bool keep = valid && lookup_bin(sigma2(ua + slo - t), a21, wB21, mg1, sh1) >= s_mmin[ud];
+      const int64_t uh = ua + slo - s_thr[ud];  // hopeless time (computed here: refilled lanes' loads
+      const bool keep = valid && t <= uh;        // are never consumed in the decision that issued them)
       const unsigned km = __ballot_sync(FULL, keep);
       const int need = kmax - wc;
       unsigned consumed = vm;
@@ -161,6 +176,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       if ((kc >> lane) & 1u) {
         const int slot = wc + __popc(kc & ((1u << lane) - 1u));
         w_dl[slot] = ua + slo;
+        w_h[slot] = uh;
         w_d[slot] = ud;
         w_tb[slot] = ut;
       }
@@ -178,9 +194,12 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         ut = st;
       } else {
         const int64_t idx = cursor + lane;
-        ua = idx < n ? arr[idx] : INT64_MAX;
-        ud = idx < n ? dis[idx] : 0;
-        ut = idx < n ? (int)tbs[idx] : 0;
+        ua = INT64_MAX;
+        if (idx < n) {
+          ua = arr[idx];
+          ud = dis[idx];
+          ut = tbs[idx];
+        }
       }
       if (nc < 32) break;
     }
@@ -197,18 +216,20 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     const int dr = mem ? w_d[lane] : 0;
     const int tb = mem ? w_tb[lane] : 0;
 
+    int kstar = 1;  // a window of one has a single candidate: no scoring needed
+    if (wc > 1) {   // warp-uniform
     float lg[BPL];
 #pragma unroll
     for (int b = 0; b < BPL; ++b) lg[b] = 0.f;
     const bool vok = lane * BPL < B;
 #pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 4) {
-      if (k0 >= wc) break;
-      __syncwarp();  // the previous group's gathers are done before its staging rows are rewritten
+    for (int k0 = 0; k0 < 32; k0 += REPLAY_KB) {  // unrolled: profile entries are immediate constants
+      if (k0 >= wc) break;                        // warp-uniform
+      if (k0 > 0) __syncwarp();                   // previous block's gathers are done
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int d = __shfl_sync(FULL, dr, k0 + i);  // beyond wc: lane >= wc holds id 0 (harmless)
-        if (vok && k0 + i < wc) {
+      for (int i = 0; i < REPLAY_KB; ++i) {
+        const int d = __shfl_sync(FULL, dr, (k0 + i) & 31);  // beyond wc: harmless id 0
+        if (vok) {
           const Vec<BPL> x = *reinterpret_cast<const Vec<BPL> *>(s_store + d * B + lane * BPL);
 #pragma unroll
           for (int e = 0; e < BPL; ++e) lg[e] += x.x[e];
@@ -217,29 +238,33 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       }
       __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int kk = k0 + i;  // k - 1
+      for (int i = 0; i < REPLAY_KB; ++i) {
+        const int kk = k0 + i;  // k - 1 (rows at or beyond wc are computed but never read)
         const int bi = lookup_bin(sig, p.prof.a2[kk], p.prof.wB2[kk], p.prof.mag[kk], p.prof.sh[kk]);
         const float pr = ex2_approx(stg[i * STG + bi - 1]);
-        Pm[kk * PST + lane] = lane <= kk ? pr : 0.f;
+        Pm[(kk & 31) * PST + lane] = lane <= kk ? pr : 0.f;
       }
     }
     __syncwarp();
-    // E_k = sum_r P[k-1][r] in lane k-1 (rows at or beyond wc are never read)
+    // E_k = sum_{r<k} P[k-1][r] in lane k-1: 128-bit row loads, adder tree
     float E = 0.f;
     if (mem) {
       const float4 *row = reinterpret_cast<const float4 *>(Pm + lane * PST);
-      for (int j = 0; 4 * j <= lane; ++j) {
-        const float4 x = row[j];
-        E += x.x;
-        E += x.y;
-        E += x.z;
-        E += x.w;
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[j] = 0.f;
+        if (4 * j <= lane) {
+          const float4 x = row[j];
+          acc[j] = (x.x + x.y) + (x.z + x.w);
+        }
       }
+      E = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
     // ---- 3. argmax + dispatch ----------------------------------------------
     const uint32_t mx = __reduce_max_sync(FULL, mem ? __float_as_uint(E) : 0u);
-    const int kstar = (int)__reduce_min_sync(FULL, (mem && __float_as_uint(E) == mx) ? (uint32_t)lane : 32u) + 1;
+    kstar = (int)__reduce_min_sync(FULL, (mem && __float_as_uint(E) == mx) ? (uint32_t)lane : 32u) + 1;
+    }
     const int mbin = (int)__reduce_max_sync(FULL, lane < kstar ? (uint32_t)tb : 0u);
     const int64_t dur = (int64_t)p.prof.a[kstar - 1] + (int64_t)p.prof.w[kstar - 1] * mbin;
     const unsigned fm = __ballot_sync(FULL, lane < kstar && t + dur <= Dr);
