@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--replay-arrivals", type=int, default=100_000)
     ap.add_argument("--replay-reps", type=int, default=2)
     ap.add_argument("--no-shard-proxy", action="store_true")
+    ap.add_argument("--no-policies", action="store_true", help="skip the replay policy-variant sweep")
+    ap.add_argument("--policy-seeds", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 workload lines")
@@ -454,6 +456,44 @@ def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True):
     return max_over_ranks(e0.elapsed_time(e1)) / reps, tables.cpu().numpy(), clk.summary()
 
 
+def run_policies(args, rank, world, dev):
+    """Replay policy variants (orloj_replay_trace_ex) on a
+    smaller sweep: finish rate per family and SLO bucket for each
+    (objective, drop rule); counters summed over ranks."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    from paper_2209_00159_b200 import parallel, policy
+
+    seeds = args.policy_seeds
+    a2 = argparse.Namespace(**vars(args))
+    a2.replay_seeds = seeds
+    fams = build_replay(a2, rank, world, dev)
+    thr = {f.tf.fam.name: torch.from_numpy(policy.expected_latency_thresholds(
+        f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).to(dev) for f in fams}
+    nb = len(gen.BUCKET_SLO_MULTS)
+    out = {"sweep": f"4 families x 8 buckets x {seeds} seeds x {args.replay_arrivals} arrivals"}
+    for objective in ("expected_finish", "finish_rate"):
+        for drop in ("hopeless", "expected_latency"):
+            tabs = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for f, t_ in zip(fams, tabs):
+                orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, objective=objective,
+                                 drop_threshold=thr[f.tf.fam.name] if drop == "expected_latency" else None)
+            e1.record()
+            parallel.allreduce_counters(tabs)
+            torch.cuda.synchronize()
+            c = tabs.cpu().numpy()
+            out[f"{objective}/{drop}"] = {
+                "ms": e0.elapsed_time(e1),
+                "finish_rate_by_bucket": {f.tf.fam.name: [round(float(x), 4) for x in c[i, :, 1] / np.maximum(c[i, :, 0], 1)]
+                                          for i, f in enumerate(fams)},
+                "dropped_frac": round(float(c[:, :, 2].sum() / max(c[:, :, 0].sum(), 1)), 4)}
+    return out
+
+
 def run_replay(args, rank, world, dev, barrier, max_over_ranks):
     import gen
 
@@ -474,6 +514,8 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
            "gpu_launches_per_sweep": len(fams), "clocks": clk,
            "collective": "one torch.distributed.all_reduce of the int64 [4 x 8 x 7] counters (NCCL) per sweep, "
                          "inside the timed region"}
+    if not args.no_policies:
+        out["policies"] = run_policies(args, rank, world, dev)
     if world == 1 and not args.no_shard_proxy:
         # strong-scaling proxy on one GPU: the time of rank 0's shard of an N-GPU run
         # (everything but the ~10 us all-reduce), and the implied speed-up

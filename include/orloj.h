@@ -202,6 +202,27 @@ orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_pr
                                 const orloj_trace *trace, orloj_counters *per_bucket,
                                 int32_t *decision_log, void *stream);
 
+/* Replay policy variants (the Alg. 1 ingredients,
+ * PAPER.md:306-373).  objective: ORLOJ_OBJ_EXPECTED_FINISH picks argmax E_k
+ * (the default of orloj_replay_trace); ORLOJ_OBJ_FINISH_RATE picks argmax
+ * E_k / E[L_{B_k}] — expected finishes per tick of worker time, the 1/E[L]
+ * factor of Eq. 1 with E[L_{B_k}] from Eq. 5 (:493-502); ties
+ * -> smallest k.  drop_threshold_ticks: device int64 [num_dists] or NULL.  A
+ * request of distribution d is dropped at time t iff D_r - t < thr[d]; NULL
+ * means the hopeless rule thr[d] = a_1 + w_1 m_min(d) (P_r(1) = 0, A16).  The
+ * Alg. 1 drop "t + EstimateBatchLatency(r, 1) > D_r" is
+ * thr[d] = a_1 + ceil(w_1 E[bin_d]) (an integer the caller computes from the
+ * histogram counts).  Thresholds are assumed non-negative and fixed per replay
+ * (dropping stays permanent only if thr[d] <= a_1 + w_1 B). */
+typedef enum { ORLOJ_OBJ_EXPECTED_FINISH = 0, ORLOJ_OBJ_FINISH_RATE = 1 } orloj_objective;
+typedef struct {
+  int32_t objective;                   /* orloj_objective */
+  const int64_t *drop_threshold_ticks; /* device [num_dists] or NULL (hopeless rule) */
+} orloj_replay_policy;
+orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency_profile *profile,
+                                   const orloj_trace *trace, const orloj_replay_policy *policy,
+                                   orloj_counters *per_bucket, int32_t *decision_log, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Validation (synchronous, O(N), not hot; may allocate a few bytes of scratch).
  * ------------------------------------------------------------------------- */

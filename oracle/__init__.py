@@ -47,7 +47,7 @@ def _load():
         lib.oracle_cdf.argtypes = [P, i32, i32, P]
         lib.oracle_score.argtypes = [P, i32, i32, P, P, i32, i64, P, P, P, P, P, P, P, P, P, i32]
         lib.oracle_bruteforce.argtypes = [P, i32, i32, P, P, i32, P, P, i64, P, P, i32]
-        lib.oracle_replay.argtypes = [P, i32, i32, P, P, i32, i64, P, P, P, P, P, P, P, P, P, i32]
+        lib.oracle_replay.argtypes = [P, i32, i32, P, P, i32, i64, P, P, P, P, P, P, P, P, P, i32, i32, i32, P]
         for f in (lib.oracle_cdf, lib.oracle_score, lib.oracle_bruteforce, lib.oracle_replay,
                   lib.oracle_max_threads):
             f.restype = ctypes.c_int32
@@ -122,10 +122,13 @@ def bruteforce(counts, a, w, deadline, dist, now, nthreads=0):
     return P, E
 
 
-def replay(F, a, w, arr_off, arrival, dist, true_bin, slo, follow_log=None, want_log=False, nthreads=0):
+def replay(F, a, w, arr_off, arrival, dist, true_bin, slo, follow_log=None, want_log=False, nthreads=0,
+           objective="expected_finish", drop="hopeless", counts=None):
     """O2.  Returns dict(counters [S,7] int64, log | None, ties [S,3]:
     (decisions, GPU choices != oracle choice, first decision outside the tie
-    set or -1))."""
+    set or -1)).  objective: "expected_finish" (argmax E_k) or "finish_rate"
+    (argmax E_k / E[L_{B_k}]); drop: "hopeless" (A16) or "expected_latency"
+    (Alg. 1, PAPER.md:351; needs `counts`)."""
     F = _c(F, np.float64)
     D, B = F.shape
     a, w = _c(a, np.int64), _c(w, np.int64)
@@ -137,8 +140,12 @@ def replay(F, a, w, arr_off, arrival, dist, true_bin, slo, follow_log=None, want
     log = np.zeros(N + S, np.int32) if want_log else None
     ties = np.zeros((S, 3), np.int64)
     fl = _c(follow_log, np.int32) if follow_log is not None else None
+    obj = {"expected_finish": 0, "finish_rate": 1}[objective]
+    dm = {"hopeless": 0, "expected_latency": 1}[drop]
+    cts = None if counts is None else _c(counts, np.uint32)
     st = _load().oracle_replay(_p(F), D, B, _p(a), _p(w), len(a), S, _p(arr_off), _p(arrival), _p(dist),
-                               _p(true_bin), _p(slo), _p(counters), _p(fl), _p(log), _p(ties), nthreads)
+                               _p(true_bin), _p(slo), _p(counters), _p(fl), _p(log), _p(ties), nthreads, obj, dm,
+                               _p(cts))
     if st:
         raise OracleError(f"oracle_replay status {st}")
     return {"counters": counters, "log": log, "ties": ties}

@@ -269,18 +269,46 @@ int32_t oracle_bruteforce(const uint32_t *counts, int32_t D, int32_t B, const in
  * Decision log layout (shared with the C-ABI): decision d of scenario s at
  * [arr_off[s] + s + d], terminated by 0.
  * ------------------------------------------------------------------------- */
+/* Drop rules.  mode 0 (A16): r is hopeless iff P_r(1) = 0 exactly, i.e. the
+ * looked-up bin i*(r,1) is 0 or F_{d_r}(tau_i*) = 0.  mode 1 (Alg. 1's drop,
+ * PAPER.md:351 with EstimateBatchLatency(r, 1) = a_1 + w_1 E[bin_r], Eq. 3 and
+ * Eq. 5 for a batch of one): drop iff t + a_1 + w_1 E[bin] > D_r, evaluated
+ * exactly in integers as (sigma - a_1) * total < w_1 * sum_i i count_i. */
+static int drop_request(const double *F, int32_t B, const int64_t *a, const int64_t *w, int64_t sigma,
+                        int32_t d, int32_t mode, const int64_t *exp_num, const int64_t *exp_den) {
+  if (mode == 0) {
+    int64_t i1 = lookup(sigma, a[0], w[0], B);
+    return (i1 == 0) || F[(int64_t)d * B + i1 - 1] == 0.0;
+  }
+  __int128 lhs = (__int128)(sigma - a[0]) * exp_den[d];
+  __int128 rhs = (__int128)w[0] * exp_num[d];
+  return lhs < rhs;
+}
+
 int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, const int64_t *w,
                       int32_t kmax, int64_t S, const int64_t *arr_off, const int64_t *arrival,
                       const int32_t *dist, const int16_t *true_bin, const int64_t *slo,
                       int64_t *counters /* [S][7] */, const int32_t *follow_log,
-                      int32_t *log_out, int64_t *tie_info /* [S][3] or NULL */, int32_t nthreads) {
+                      int32_t *log_out, int64_t *tie_info /* [S][3] or NULL */, int32_t nthreads,
+                      int32_t objective /* 0: E_k, 1: E_k / E[L_{B_k}] */,
+                      int32_t drop_mode /* 0: hopeless (A16), 1: expected latency (Alg. 1) */,
+                      const uint32_t *counts /* [D][B], needed for drop_mode 1 */) {
   if (kmax < 1 || B < 1 || S < 0) return OR_EINVAL;
-  (void)D;
+  if (drop_mode == 1 && !counts) return OR_EINVAL;
   set_threads(nthreads);
+  int64_t *exp_num = (int64_t *)calloc((size_t)D + 1, sizeof(int64_t));
+  int64_t *exp_den = (int64_t *)calloc((size_t)D + 1, sizeof(int64_t));
+  if (drop_mode == 1)
+    for (int64_t d = 0; d < D; ++d)
+      for (int32_t i = 0; i < B; ++i) {
+        exp_num[d] += (int64_t)(i + 1) * counts[d * B + i]; /* sum_i i count_i (tau_i = i bins) */
+        exp_den[d] += counts[d * B + i];
+      }
 #pragma omp parallel
   {
     double *G = (double *)malloc(sizeof(double) * (B + 1));
     double *E = (double *)malloc(sizeof(double) * kmax);
+    double *EL = (double *)malloc(sizeof(double) * kmax);
     int64_t *win = (int64_t *)malloc(sizeof(int64_t) * kmax);
     int64_t *carry = (int64_t *)malloc(sizeof(int64_t) * kmax);
     int64_t *wdl = (int64_t *)malloc(sizeof(int64_t) * kmax);
@@ -300,16 +328,16 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
         int32_t wc = 0;
         for (int32_t c = 0; c < ncarry; ++c) {
           int64_t r = carry[c];
-          int64_t i1 = lookup(arrival[base + r] + slo[s] - t, a[0], w[0], B);
-          int hopeless = (i1 == 0) || F[(int64_t)dist[base + r] * B + i1 - 1] == 0.0;
-          if (hopeless) ++c_drop;
+          if (drop_request(F, B, a, w, arrival[base + r] + slo[s] - t, dist[base + r], drop_mode, exp_num,
+                           exp_den))
+            ++c_drop;
           else win[wc++] = r;
         }
         while (wc < kmax && cursor < n && arrival[base + cursor] <= t) {
           int64_t r = cursor++;
-          int64_t i1 = lookup(arrival[base + r] + slo[s] - t, a[0], w[0], B);
-          int hopeless = (i1 == 0) || F[(int64_t)dist[base + r] * B + i1 - 1] == 0.0;
-          if (hopeless) ++c_drop;
+          if (drop_request(F, B, a, w, arrival[base + r] + slo[s] - t, dist[base + r], drop_mode, exp_num,
+                           exp_den))
+            ++c_drop;
           else win[wc++] = r;
         }
         ncarry = 0;
@@ -318,12 +346,25 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
           wdl[j] = arrival[base + win[j]] + slo[s];
           wd[j] = dist[base + win[j]];
         }
-        int32_t ko = score_window(F, B, a, w, wc, wdl, wd, t, E, NULL, NULL, G);
+        int32_t ko = score_window(F, B, a, w, wc, wdl, wd, t, E, NULL, objective ? EL : NULL, G);
+        if (objective) {
+          /* finish-rate objective: argmax E_k / E[L_{B_k}] (Eq. 1's 1/E[L], Eq. 5), ties -> smallest k */
+          ko = 1;
+          for (int32_t kk = 1; kk <= wc; ++kk) {
+            E[kk - 1] = E[kk - 1] / EL[kk - 1];
+            if (E[kk - 1] > E[ko - 1]) ko = kk;
+          }
+        }
         int32_t k = ko;
         if (follow_log) {
           int32_t kg = follow_log[base + s + ndec];
           double emax = E[ko - 1];
-          int ok = kg >= 1 && kg <= wc && E[kg - 1] >= emax - 1e-5 * (double)(ko + kg);
+          /* tie band: E_k within 1e-5 k; for the rate, relative 1e-4 (E[L] error) plus the E band over E[L] */
+          double band = objective ? 1e-4 * emax + 1e-5 * (double)(ko + kg) /
+                                                      (kg >= 1 && kg <= wc && EL[kg - 1] < EL[ko - 1] ? EL[kg - 1]
+                                                                                                     : EL[ko - 1])
+                                  : 1e-5 * (double)(ko + kg);
+          int ok = kg >= 1 && kg <= wc && E[kg - 1] >= emax - band;
           if (!ok && first_bad < 0) first_bad = ndec;
           if (kg != ko) ++nties;
           if (kg >= 1 && kg <= wc) k = kg;
@@ -364,6 +405,9 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
     free(carry);
     free(wdl);
     free(wd);
+    free(EL);
   }
+  free(exp_num);
+  free(exp_den);
   return OR_OK;
 }

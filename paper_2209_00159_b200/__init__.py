@@ -306,10 +306,17 @@ class Trace:
         return ctypes.byref(self._c)
 
 
+OBJECTIVES = {"expected_finish": 0, "finish_rate": 1}
+
+
 def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, per_bucket=None,
-                 decision_log: bool | torch.Tensor = False, stream=None):
+                 decision_log: bool | torch.Tensor = False, stream=None, objective: str = "expected_finish",
+                 drop_threshold: Optional[torch.Tensor] = None):
     """Replay every scenario; returns (per_bucket int64 [num_buckets, 7], log or None).
-    per_bucket is ADDED to (pass a zeroed tensor to accumulate across calls)."""
+    per_bucket is ADDED to (pass a zeroed tensor to accumulate across calls).
+    objective: "expected_finish" (argmax E_k) or "finish_rate" (argmax
+    E_k / E[L_{B_k}]); drop_threshold: device int64 [num_dists] (see
+    policy.expected_latency_thresholds) or None for the hopeless rule."""
     dev = trace.arrival.device
     if per_bucket is None:
         per_bucket = torch.zeros((trace.num_buckets, 7), dtype=torch.int64, device=dev)
@@ -319,6 +326,13 @@ def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, p
         log = _dev(decision_log, torch.int32, "decision_log")
     elif decision_log:
         log = torch.zeros(trace.num_arrivals + trace.num_scenarios, dtype=torch.int32, device=dev)
-    _abi.check(_abi.lib().orloj_replay_trace(store.c(), profile.c(), trace.c(), per_bucket.data_ptr(), _ptr(log),
-                                             _stream_ptr(stream)))
+    if objective not in OBJECTIVES:
+        raise OrlojError(1, f"objective must be one of {sorted(OBJECTIVES)}")
+    if drop_threshold is not None:
+        _dev(drop_threshold, torch.int64, "drop_threshold")
+        if drop_threshold.numel() != store.num_dists:
+            raise OrlojError(1, "drop_threshold must have one entry per distribution")
+    pol = _abi.ReplayPolicyC(OBJECTIVES[objective], _ptr(drop_threshold))
+    _abi.check(_abi.lib().orloj_replay_trace_ex(store.c(), profile.c(), trace.c(), ctypes.byref(pol),
+                                                per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
     return per_bucket, log

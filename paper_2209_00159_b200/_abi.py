@@ -57,6 +57,10 @@ class TraceC(ctypes.Structure):
                 ("slo_ticks", ctypes.c_void_p), ("bucket", ctypes.c_void_p), ("num_buckets", ctypes.c_int32)]
 
 
+class ReplayPolicyC(ctypes.Structure):
+    _fields_ = [("objective", ctypes.c_int32), ("drop_threshold_ticks", ctypes.c_void_p)]
+
+
 class Counters(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("total", "finished", "dropped", "late", "batches", "busy_ticks", "span_ticks")]
@@ -77,6 +81,8 @@ SIGNATURES = {
                                              _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "orloj_replay_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
                                           ctypes.POINTER(TraceC), _P, _P, _P]),
+    "orloj_replay_trace_ex": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                             ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC), _P, _P, _P]),
     "orloj_validate_store": (ctypes.c_int, [ctypes.POINTER(Store), _P]),
     "orloj_validate_queues": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC), _P]),
     "orloj_validate_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(TraceC), _P]),

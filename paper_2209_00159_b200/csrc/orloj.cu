@@ -302,8 +302,18 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
 
 orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
                                 const orloj_trace *tr, orloj_counters *per_bucket, int32_t *log, void *stream) {
+  const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr};
+  return orloj_replay_trace_ex(store, profile, tr, &def, per_bucket, log, stream);
+}
+
+orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency_profile *profile,
+                                   const orloj_trace *tr, const orloj_replay_policy *policy,
+                                   orloj_counters *per_bucket, int32_t *log, void *stream) {
   orloj_status st;
   if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
+  if (!policy || (policy->objective != ORLOJ_OBJ_EXPECTED_FINISH && policy->objective != ORLOJ_OBJ_FINISH_RATE))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay policy: objective must be EXPECTED_FINISH or FINISH_RATE");
+  const bool rate = policy->objective == ORLOJ_OBJ_FINISH_RATE;
   if (!tr || tr->num_scenarios < 0 || tr->num_buckets < 1)
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace: need num_scenarios >= 0 and num_buckets >= 1");
   if (tr->num_scenarios > 0 && (!tr->arrival_offsets || !tr->arrival_ticks || !tr->dist_id || !tr->true_bin ||
@@ -317,8 +327,10 @@ orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_pr
   const size_t store_b = (size_t)D * B * 4;
   if (store_b > (64u << 10))
     return fail(ORLOJ_ERR_CAPACITY, "replay: store of %zu bytes exceeds the 64 KiB shared-memory budget", store_b);
-  const size_t warp_b = bpl == 1 ? ReplayWarpSmem<1>::bytes() : bpl == 2 ? ReplayWarpSmem<2>::bytes()
-                                                                          : ReplayWarpSmem<4>::bytes();
+  const size_t warp_b = rate ? (bpl == 1 ? ReplayWarpSmem<1, true>::bytes()
+                                         : bpl == 2 ? ReplayWarpSmem<2, true>::bytes() : ReplayWarpSmem<4, true>::bytes())
+                             : (bpl == 1 ? ReplayWarpSmem<1>::bytes()
+                                         : bpl == 2 ? ReplayWarpSmem<2>::bytes() : ReplayWarpSmem<4>::bytes());
   const size_t smem = replay_head_bytes(D, B) + REPLAY_WARPS * warp_b;
   p.log2F = store->log2_cdf;
   p.D = D;
@@ -332,23 +344,26 @@ orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_pr
   p.bucket = tr->bucket;
   p.counters = reinterpret_cast<unsigned long long *>(per_bucket);
   p.log = log;
+  p.drop_thr = policy->drop_threshold_ticks;
   if (p.S == 0) return ok();
   const unsigned blocks = (unsigned)((p.S + REPLAY_WARPS - 1) / REPLAY_WARPS);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  switch (bpl) {
-    case 1:
-      e = cudaFuncSetAttribute(replay_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) replay_kernel<1><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);
-      break;
-    case 2:
-      e = cudaFuncSetAttribute(replay_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) replay_kernel<2><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);
-      break;
+  switch (bpl * 2 + (rate ? 1 : 0)) {
+#define ORLOJ_REPLAY_CASE(BPL_, RATE_)                                                                         \
+  case BPL_ * 2 + (RATE_ ? 1 : 0):                                                                             \
+    e = cudaFuncSetAttribute(replay_kernel<BPL_, RATE_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e == cudaSuccess) replay_kernel<BPL_, RATE_><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);               \
+    break;
+    ORLOJ_REPLAY_CASE(1, false)
+    ORLOJ_REPLAY_CASE(1, true)
+    ORLOJ_REPLAY_CASE(2, false)
+    ORLOJ_REPLAY_CASE(2, true)
+    ORLOJ_REPLAY_CASE(4, false)
+    ORLOJ_REPLAY_CASE(4, true)
+#undef ORLOJ_REPLAY_CASE
     default:
-      e = cudaFuncSetAttribute(replay_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess) replay_kernel<4><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);
-      break;
+      return fail(ORLOJ_ERR_CAPACITY, "replay: unsupported bins per lane");
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_trace launch");

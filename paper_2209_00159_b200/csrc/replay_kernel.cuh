@@ -40,6 +40,7 @@ struct ReplayParams {
   const int32_t *bucket;
   unsigned long long *counters;  // [num_buckets][7]
   int32_t *log;                  // [N + S] or null
+  const int64_t *drop_thr;       // [D] or null: drop iff D_r - t < thr[d_r] (null: hopeless rule)
   ProfileDev prof;
 };
 
@@ -51,11 +52,14 @@ constexpr int REPLAY_KB = ORLOJ_REPLAY_KB;  // candidate sizes per scoring block
 
 // Per-warp shared memory: REPLAY_KB staging rows, the window's member fields
 // and the P[k][r] matrix (row stride 36 floats: conflict-free 128-bit reads).
-template <int BPL>
+// RATE (finish-rate objective) adds the S[k][lane] matrix of per-lane partial
+// sums of G_k over the bins, for E[L_{B_k}].
+template <int BPL, bool RATE = false>
 struct ReplayWarpSmem {
   static constexpr int STG = 32 * BPL + 4;
   static constexpr int PSTRIDE = 36;
-  static constexpr size_t BYTES = (size_t)(REPLAY_KB * STG) * 4 + 32 * (8 + 8 + 4 + 4) + 32 * PSTRIDE * 4;
+  static constexpr size_t BYTES = (size_t)(REPLAY_KB * STG) * 4 + 32 * (8 + 8 + 4 + 4) +
+                                  (RATE ? 2 : 1) * 32 * PSTRIDE * 4;
   __host__ __device__ static constexpr size_t bytes() { return BYTES; }
 };
 
@@ -68,11 +72,11 @@ __host__ __device__ inline size_t replay_head_bytes(int D, int B) {
 #define ORLOJ_REPLAY_MIN_BLOCKS 8
 #endif
 
-template <int BPL>
+template <int BPL, bool RATE>
 __global__ void __launch_bounds__(REPLAY_WARPS * 32, ORLOJ_REPLAY_MIN_BLOCKS)
 replay_kernel(const __grid_constant__ ReplayParams p) {
-  constexpr int STG = ReplayWarpSmem<BPL>::STG;
-  constexpr int PST = ReplayWarpSmem<BPL>::PSTRIDE;
+  constexpr int STG = ReplayWarpSmem<BPL, RATE>::STG;
+  constexpr int PST = ReplayWarpSmem<BPL, RATE>::PSTRIDE;
 
   extern __shared__ __align__(16) float s_dyn[];
   const int D = p.D, B = p.B;
@@ -81,13 +85,14 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   char *s_warp = reinterpret_cast<char *>(s_dyn) + replay_head_bytes(D, B);
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  char *my = s_warp + wid * ReplayWarpSmem<BPL>::bytes();
+  char *my = s_warp + wid * ReplayWarpSmem<BPL, RATE>::bytes();
   float *stg = reinterpret_cast<float *>(my) + 4;                            // REPLAY_KB rows, stride STG
   int64_t *w_dl = reinterpret_cast<int64_t *>(my + REPLAY_KB * STG * 4);    // window deadlines
   int64_t *w_h = w_dl + 32;                                                 // window hopeless times
   int32_t *w_d = reinterpret_cast<int32_t *>(w_h + 32);                     // window distributions
   int32_t *w_tb = w_d + 32;                                                 // window true bins
   float *Pm = reinterpret_cast<float *>(w_tb + 32);                         // P[k-1][r], stride PST
+  float *Sm = Pm + 32 * PST;  // RATE only: per-lane partial sum_{i<B} G_k(tau_i), [k-1][lane]
 
   // stage the (small) store; hopeless threshold a_1 + w_1 m_min(d) per distribution
   for (int e = threadIdx.x; e < D * B; e += blockDim.x) s_store[e] = p.log2F[e];
@@ -96,7 +101,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     int m = B;
     for (int i = B - 1; i >= 0; --i)
       if (s_store[d * B + i] != -INFINITY) m = i + 1;
-    s_thr[d] = (int64_t)p.prof.a[0] + (int64_t)p.prof.w[0] * m;
+    s_thr[d] = p.drop_thr ? p.drop_thr[d] : (int64_t)p.prof.a[0] + (int64_t)p.prof.w[0] * m;
   }
   if (lane < REPLAY_KB) stg[lane * STG - 1] = -INFINITY;
   __syncthreads();
@@ -111,6 +116,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int64_t *arr = p.arrival + base;
   const int32_t *dis = p.dist + base;
   const int16_t *tbs = p.true_bin + base;
+  // RATE: lane k-1 evaluates E[L_{B_k}] with a_k, w_k of its own candidate size
+  const float my_a = RATE ? (float)p.prof.a[lane] : 0.f;
+  const float my_w = RATE ? (float)p.prof.w[lane] : 0.f;
 
   int64_t t = INT64_MIN;
   int64_t cursor = 0;
@@ -235,6 +243,14 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
           for (int e = 0; e < BPL; ++e) lg[e] += x.x[e];
         }
         st_vec<BPL>(stg + i * STG + lane * BPL, lg);
+        if constexpr (RATE) {
+          // this lane's share of sum_{i<B} G_k(tau_i) (bins tau_1 .. tau_{B-1})
+          float part = 0.f;
+#pragma unroll
+          for (int e = 0; e < BPL; ++e)
+            if (lane * BPL + e < B - 1) part += ex2_approx(lg[e]);
+          Sm[((k0 + i) & 31) * PST + lane] = part;
+        }
       }
       __syncwarp();
 #pragma unroll
@@ -260,6 +276,18 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         }
       }
       E = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+      if constexpr (RATE) {
+        // finish rate E_k / E[L_{B_k}], E[L_{B_k}] = a_k + w_k (B - sum_{i<B} G_k(tau_i))  (Eq. 5)
+        const float4 *srow = reinterpret_cast<const float4 *>(Sm + lane * PST);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 x = srow[j];
+          acc[j] = (x.x + x.y) + (x.z + x.w);
+        }
+        const float S = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        const float EL = my_a + my_w * ((float)B - S);
+        E = E / EL;
+      }
     }
     // ---- 3. argmax + dispatch ----------------------------------------------
     const uint32_t mx = __reduce_max_sync(FULL, mem ? __float_as_uint(E) : 0u);

@@ -120,3 +120,62 @@ def test_replay_empty_and_single():
     assert r["counters"][0].tolist() == [0] * 7
     assert r["counters"][1].tolist() == [1, 1, 0, 0, 1, 4, 4]
     assert r["log"].tolist() == [0, 1, 0]
+
+
+# ---------------------------------------------------------------------------
+# replay policy variants
+# ---------------------------------------------------------------------------
+import _policy_cases  # noqa: E402
+
+
+@pytest.mark.parametrize("case", _policy_cases.load(), ids=lambda c: c["name"])
+def test_policy_golden(case):
+    x = _policy_cases.arrays(case)
+    F = oracle.cdf(x["counts"])
+    for key, exp in case["expect"].items():
+        objective, drop = key.split("/")
+        r = oracle.replay(F, x["a"], x["w"], x["off"], x["arrival"], x["dist"], x["tb"], x["slo"],
+                          objective=objective, drop=drop, counts=x["counts"])
+        assert dict(zip(oracle.COUNTER_FIELDS, r["counters"][0].tolist())) == exp, key
+
+
+def test_expected_latency_thresholds_exact():
+    """policy.expected_latency_thresholds implements t + a_1 + w_1 E[bin] > D_r
+    exactly: check the equivalence D - t < thr  <=>  (D - t - a_1) total <
+    w_1 sum_i i c_i (exact rationals) around every threshold."""
+    from paper_2209_00159_b200 import policy
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        B = int(rng.integers(4, 65))
+        counts = rng.integers(0, 1000, (3, B)).astype(np.uint32)
+        counts[:, -1] += 1
+        a = np.array([int(rng.integers(0, 5000))], np.int64)
+        w = np.array([int(rng.integers(1, 3000))], np.int64)
+        thr = policy.expected_latency_thresholds(counts, a, w)
+        for d in range(3):
+            num = sum((i + 1) * int(c) for i, c in enumerate(counts[d]))
+            den = int(counts[d].sum())
+            for slack in range(int(thr[d]) - 3, int(thr[d]) + 3):
+                assert (slack < thr[d]) == ((slack - int(a[0])) * den < int(w[0]) * num)
+        assert (policy.hopeless_thresholds(counts, a, w) == a[0] + w[0] * (np.argmax(counts > 0, 1) + 1)).all()
+
+
+@pytest.mark.parametrize("fam", ["skipnet", "gpt"])
+def test_policy_invariants(fam):
+    tf = gen.c5_trace_family(fam)
+    off, arr, dist, tb, slo = _small_trace(tf, S=8, n=1500)
+    F = oracle.cdf(tf.fam.counts)
+    for objective in ("expected_finish", "finish_rate"):
+        for drop in ("hopeless", "expected_latency"):
+            r = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo, want_log=True,
+                              objective=objective, drop=drop, counts=tf.fam.counts)
+            c = r["counters"]
+            assert (c[:, 1] + c[:, 2] + c[:, 3] == c[:, 0]).all()
+            r2 = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo, follow_log=r["log"],
+                               objective=objective, drop=drop, counts=tf.fam.counts)
+            assert (r2["counters"] == c).all() and (r2["ties"][:, 2] == -1).all()
+    # the expected-latency rule drops at least what the hopeless rule drops
+    h = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo)["counters"]
+    e = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo, drop="expected_latency",
+                      counts=tf.fam.counts)["counters"]
+    assert e[:, 2].sum() >= h[:, 2].sum()
