@@ -93,6 +93,19 @@ typedef struct {
 orloj_status orloj_store_build(const uint32_t *counts, int32_t num_dists, int32_t num_bins,
                                float *log2_cdf_out, void *stream);
 
+/* Online profiler: accumulate sampled
+ * solo execution times into the integer histogram counts a store is built
+ * from.  Sample j (distribution dist_id[j], solo time solo_ticks[j] >= 0) adds
+ * 1 to counts[d][i-1] with i = clamp(ceil(solo / bin_ticks), 1, B) — bin i
+ * holds (tau_{i-1}, tau_i] ("discrete at upper edges", A1; longer times fold
+ * into bin B).  counts: device uint32 [D][B], ADDED to (atomics); the window
+ * reset of the paper is a memset of counts by the caller, followed by
+ * orloj_store_build.  Async on `stream`.  Errors: INVALID_ARGUMENT (sizes,
+ * bin_ticks <= 0), CUDA.  Samples with dist_id outside [0, D) are ignored. */
+orloj_status orloj_histogram_accumulate(const int32_t *dist_id, const int64_t *solo_ticks, int64_t num_samples,
+                                        int64_t bin_ticks, uint32_t *counts, int32_t num_dists, int32_t num_bins,
+                                        void *stream);
+
 /* ---------------------------------------------------------------------------
  * Latency profile: Eq. 3 generalised to a monotone integer table (A3).
  * A batch of k whose slowest member lies in bin m runs a_k + w_k * m ticks.

@@ -102,6 +102,36 @@ class HistogramStore:
         return ctypes.byref(self._c)
 
 
+class Profiler:
+    """Online profiler: sampled solo execution times are
+    accumulated on the GPU into integer histogram counts (orloj_histogram_
+    accumulate); `refresh` rebuilds the store rows from them, `reset` starts a
+    new profiling window."""
+
+    def __init__(self, num_dists: int, num_bins: int, bin_ticks: int, device="cuda"):
+        self.counts = torch.zeros((num_dists, num_bins), dtype=torch.int32, device=device)
+        self.bin_ticks = int(bin_ticks)
+
+    def add(self, dist_id: torch.Tensor, solo_ticks: torch.Tensor, stream=None):
+        _dev(dist_id, torch.int32, "dist_id")
+        _dev(solo_ticks, torch.int64, "solo_ticks")
+        if dist_id.numel() != solo_ticks.numel():
+            raise OrlojError(1, "dist_id and solo_ticks must have the same length")
+        D, B = self.counts.shape
+        _abi.check(_abi.lib().orloj_histogram_accumulate(dist_id.data_ptr(), solo_ticks.data_ptr(), dist_id.numel(),
+                                                         self.bin_ticks, self.counts.data_ptr(), D, B,
+                                                         _stream_ptr(stream)))
+        return self
+
+    def reset(self):
+        self.counts.zero_()
+        return self
+
+    def refresh(self, store: "HistogramStore", stream=None) -> "HistogramStore":
+        """Rebuild every row of `store` from the current window (synchronises)."""
+        return store.build_rows(self.counts, 0, stream)
+
+
 # ----------------------------------------------------------------------------
 # latency profile (Eq. 3 generalised, DESIGN.md A3)
 # ----------------------------------------------------------------------------

@@ -83,6 +83,8 @@ SIGNATURES = {
                                           ctypes.POINTER(TraceC), _P, _P, _P]),
     "orloj_replay_trace_ex": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
                                              ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC), _P, _P, _P]),
+    "orloj_histogram_accumulate": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int32,
+                                                  ctypes.c_int32, _P]),
     "orloj_validate_store": (ctypes.c_int, [ctypes.POINTER(Store), _P]),
     "orloj_validate_queues": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC), _P]),
     "orloj_validate_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(TraceC), _P]),

@@ -370,6 +370,23 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
   return ok();
 }
 
+orloj_status orloj_histogram_accumulate(const int32_t *dist_id, const int64_t *solo_ticks, int64_t n,
+                                        int64_t bin_ticks, uint32_t *counts, int32_t D, int32_t B, void *stream) {
+  if (n < 0 || D < 1 || B < 1 || bin_ticks <= 0 || !counts || (n > 0 && (!dist_id || !solo_ticks)))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "histogram_accumulate: bad sizes or pointers");
+  if ((int64_t)D * B > (1ll << 30)) return fail(ORLOJ_ERR_CAPACITY, "histogram_accumulate: D*B too large");
+  if (n == 0) return ok();
+  const size_t hb = (size_t)D * B * 4;
+  const int use_smem = hb <= (48u << 10);
+  const int64_t want = (n + 255) / 256;
+  const unsigned blocks = (unsigned)(want < 148 * 8 ? want : 148 * 8);
+  hist_accumulate_kernel<<<blocks, 256, use_smem ? hb : 0, (cudaStream_t)stream>>>(dist_id, solo_ticks, n, bin_ticks,
+                                                                                    counts, D, B, use_smem);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "histogram_accumulate launch");
+  return ok();
+}
+
 orloj_status orloj_validate_store(const orloj_store *store, void *stream) {
   orloj_status st;
   if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;

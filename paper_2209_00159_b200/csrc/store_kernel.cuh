@@ -44,6 +44,36 @@ __global__ void store_build_kernel(const uint32_t *__restrict__ counts, int32_t 
   }
 }
 
+// Online profiler: sample j adds 1 to counts[d][i-1],
+// i = clamp(ceil(solo / bin_ticks), 1, B) (upper-edge bins, A1).  A CTA-private
+// histogram in shared memory when it fits, flushed with one atomic per
+// non-zero counter; otherwise global atomics.
+__global__ void hist_accumulate_kernel(const int32_t *__restrict__ dist, const int64_t *__restrict__ solo,
+                                       int64_t n, int64_t bin_ticks, uint32_t *__restrict__ counts, int32_t D,
+                                       int32_t B, int use_smem) {
+  extern __shared__ uint32_t s_h[];
+  const int DB = D * B;
+  if (use_smem) {
+    for (int e = threadIdx.x; e < DB; e += blockDim.x) s_h[e] = 0;
+    __syncthreads();
+  }
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int d = dist[j];
+    if (d < 0 || d >= D) continue;
+    const int64_t x = solo[j];
+    int64_t i = x <= 0 ? 1 : (x + bin_ticks - 1) / bin_ticks;
+    i = i < 1 ? 1 : (i > B ? B : i);
+    const int e = d * B + (int)i - 1;
+    if (use_smem) atomicAdd(&s_h[e], 1u);
+    else atomicAdd(&counts[e], 1u);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < DB; e += blockDim.x)
+      if (s_h[e]) atomicAdd(&counts[e], s_h[e]);
+  }
+}
+
 // flags: bit0 = value / shape violation, bit1 = order violation
 __global__ void validate_store_kernel(const float *__restrict__ F, int32_t D, int32_t B,
                                       unsigned int *flags) {
