@@ -398,7 +398,63 @@ def run_other_workloads(args, dev, max_over_ranks, world):
                      "timing": f"{iters} x " + (f"CUDA graph of {reps} picks" if reps > 1 else "1 pick")}
         del store, qs
     torch.cuda.empty_cache()
+    out["P1"] = run_priority(dev, max_over_ranks, world)
     return out
+
+
+def run_priority(dev, max_over_ranks, world):
+    """P1: one step = Eq. 1-2 log-priority of every queued
+    request for every batch size 1..32 (orloj_priority_scores, [32][N] fp32
+    out) + PopBatch of 32 per queue (orloj_pop_batch).  The per-size tables
+    are built once, off the critical path, outside the timing."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+
+    cfg = gen.config_priority()
+    S = cfg.kmax
+    store = wl.score_store(cfg, dev)
+    prof = wl.profile(cfg.profile)
+    qs = wl.device_queues(cfg.queues, dev, with_arrival=False)
+    Q, N = cfg.queues.Q, cfg.queues.N
+    tab = orj.PriorityTable(store, prof, S, 1.0 / cfg.fam.mean_ticks())
+    lp = torch.empty((S, N), dtype=torch.float32, device=dev)
+    bs = torch.full((Q,), S, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            tab.scores(qs, lp, stream)
+            sel = tab.pop(qs, lp, bs, stream)
+        iters = 20
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * iters + 1)]
+        ev[0].record(stream)
+        for it in range(iters):
+            tab.scores(qs, lp, stream)
+            ev[2 * it + 1].record(stream)
+            tab.pop(qs, lp, bs, stream, out=sel)
+            ev[2 * it + 2].record(stream)
+    torch.cuda.synchronize()
+    ms_sc = max_over_ranks(sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(iters)) / iters)
+    ms_pop = max_over_ranks(sum(ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(iters)) / iters)
+    ms = ms_sc + ms_pop
+    sc_bytes = N * (8 + 4 * S) + Q * (8 + 8)            # deadline in, S log p out; offsets, now
+    pop_bytes = N * 4 + Q * (8 + 4 + 32 * 4)            # one size row in; offsets, bs, selection out
+    peak, peak_src = measured_peaks()
+    del store, qs, lp
+    torch.cuda.empty_cache()
+    return {"workload": "P1: Eq. 1-2 priorities, SkipNet-like 8-app mix (B 64), 65,536 queues x 256, "
+                        "batch sizes 1..32, b = 1 / mean latency; PopBatch of 32 per queue",
+            "requests": N, "sizes": S, "ms_per_step": ms, "ms_scores": ms_sc, "ms_pop": ms_pop,
+            "scores_per_s": world * N * S / (ms / 1e3), "queues_per_s": world * Q / (ms / 1e3),
+            "roofline_scores": {"bound": "hbm", "achieved": sc_bytes / (ms_sc / 1e3) / 1e9, "peak": peak,
+                                "unit": "GB/s", "frac": sc_bytes / (ms_sc / 1e3) / 1e9 / peak,
+                                "algorithmic_bytes_per_launch": sc_bytes, "peak_source": peak_src},
+            "roofline_pop": {"bound": "hbm", "achieved": pop_bytes / (ms_pop / 1e3) / 1e9, "peak": peak,
+                             "unit": "GB/s", "frac": pop_bytes / (ms_pop / 1e3) / 1e9 / peak,
+                             "algorithmic_bytes_per_launch": pop_bytes},
+            "timing": f"{iters} steps, CUDA events around each kernel on its stream"}
 
 
 def build_replay(args, rank, world, dev):

@@ -316,6 +316,17 @@ def config2(Q: int = 1024, n: int = 64, kmax: int = 32) -> ScoreConfig:
     return ScoreConfig("C2", fam, prof, q)
 
 
+def config_priority(Q: int = 65536, n: int = 256, sizes: int = 32) -> ScoreConfig:
+    """P1: Eq. 1-2 priorities of every queued request for
+    batch sizes 1..32 over the SkipNet-like application mix (8 apps, B 64), the
+    C3 queue shape (65,536 queues x 256 requests)."""
+    seed = SEED_BASE + 6
+    fam = skipnet_family(seed)
+    prof = eq3_half(fam, sizes)
+    q = snapshot_queues(seed, np.full(Q, n), fam.p99_ticks(), D=fam.D)
+    return ScoreConfig("P1", fam, prof, q)
+
+
 def config3(Q: int = 65536, n: int = 256, kmax: int = 256, T: int = 4096, instance: int = 0) -> ScoreConfig:
     """Per-request rows: row ids are a seeded random permutation of [0, Q*n), so
     every candidate is a true 1 KB gather.  `instance` selects an

@@ -237,6 +237,50 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
                                    orloj_counters *per_bucket, int32_t *decision_log, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Eq. 1-2 priority scores and PopBatch (PAPER.md:423-455,
+ * :585-593, Alg. 1 :306-373).
+ *
+ * Batch latency of size bs (1..num_sizes): a batch of bs requests drawn from
+ * the mixture of all application distributions (weights) has its
+ * latency in bin i = (l1, l2] = (a_bs + w_bs (i-1), a_bs + w_bs i] with
+ * probability pm_i = F_mix(tau_i)^bs - F_mix(tau_{i-1})^bs (Eq. 3-4, Eq. 6
+ * i.i.d., A1 grid), uniform within the bin (the histogram of Eq. 2, frequency
+ * h_i = pm_i / w_bs).  The priority of a request with slack sigma = D_r - t is
+ * Eq. 1 with the step cost (c = 1) and an Exp(b) delay, summed per bin as
+ * Eq. 2:
+ *   p = (1 / E[L_bs]) sum_i { (h_i/b)(e^{b l2} - e^{b l1}) e^{-b sigma}   l2 <= sigma
+ *                             (h_i/b)(1 - e^{-b (sigma - l1)})            l1 < sigma < l2
+ *                             0                                           sigma <= l1 }
+ * with E[L_bs] = sum_i pm_i (l1 + l2) / 2.  Scores are returned as log p
+ * (fp32; -inf when no outcome meets the deadline).
+ * ------------------------------------------------------------------------- */
+/* Build the per-size tables (off the critical path; synchronous).
+ * log_table: device double [num_sizes][2][B+1]; [s][0][i] = log of the
+ * full-bin sum over bins 1..i divided by e^{-b sigma} (-inf at i = 0),
+ * [s][1][i] = log(h_i / b) (-inf when pm_i = 0 and at i = 0).  log_expected:
+ * device double [num_sizes], log E[L_bs].  weights: device float [D] (>= 0,
+ * not all 0) or NULL (uniform).  b_per_tick > 0 with b_per_tick * w_bs small
+ * enough that e^{b w} is finite (b w < 709).  num_sizes <= profile.kmax. */
+orloj_status orloj_priority_table(const orloj_store *store, const orloj_latency_profile *profile,
+                                  int32_t num_sizes, const float *weights, double b_per_tick,
+                                  double *log_table, double *log_expected, void *stream);
+/* log p for every queue member and batch size: device float [num_sizes][N]
+ * (size-major), N = queue_offsets[Q] - queue_offsets[0].  Uses only
+ * queue_offsets, deadline_ticks and now_ticks.  Async on stream. */
+orloj_status orloj_priority_scores(const orloj_store *store, const orloj_latency_profile *profile,
+                                   int32_t num_sizes, double b_per_tick, const double *log_table,
+                                   const double *log_expected, const orloj_queues *queues, float *log_priority,
+                                   void *stream);
+/* PopBatch: per queue q, the (up to) batch_size[q] <= 32 members with the
+ * highest log p for that size (ties -> earlier member; -inf and NaN never
+ * chosen), among the first 256 members; log_priority is the [num_sizes][N]
+ * output of orloj_priority_scores.  selected: device int32 [Q][32],
+ * member index within the queue, highest priority first, -1 after the last
+ * (a batch_size outside [1, num_sizes] selects nothing).  Async on stream. */
+orloj_status orloj_pop_batch(const orloj_queues *queues, const float *log_priority, int32_t num_sizes,
+                             const int32_t *batch_size, int32_t *selected, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Validation (synchronous, O(N), not hot; may allocate a few bytes of scratch).
  * ------------------------------------------------------------------------- */
 /* rows non-decreasing, <= 0, no NaN, [d][B-1] == 0.0f.  INVALID_ARGUMENT otherwise. */

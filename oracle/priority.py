@@ -1,0 +1,106 @@
+"""ORACLE — test infrastructure only (never on the product path).
+
+Plain fp64 numpy implementation of the Eq. 1-2 priority score of a request
+under batching (PAPER.md:423-455 Eq. 1-2, :571-593 batch latency / batch
+formation) and of PopBatch (Alg. 1): SURVEY §8(f) item 2.
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` may import it;
+it shares no code with ``paper_2209_00159_b200``.
+
+Readings (R10-R12):
+  * L of a request is the latency of its whole batch.  For batch
+    size bs the batch is bs i.i.d. draws from the mixture of all application
+    distributions of the model, so F_L = F_mix^bs (Eq. 6), with
+    the A1 grid: bin i of L_bs is (l1, l2] = (a + w(i-1), a + w i].
+  * Eq. 2 treats each histogram bin as a uniform density h = pm_i / w over
+    its range (the paper's "frequency h" must be a density for Eq. 2 to be
+    E[C_delay] - E[C_now]; the pins below check exactly that).
+  * Cost c = 1 for every request (one SLO class); E[L] is the mean
+    of the same histogram, sum_i pm_i (l1 + l2) / 2.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def mixture_cdf(counts, weights=None, store_fp32=False) -> np.ndarray:
+    """F_mix(tau_i) for i = 1..B: the weighted mixture of the applications'
+    histogram CDFs ("all execution time distributions associated
+    with the model").  counts [D][B] (every row with a positive total).
+    store_fp32: read each F_d through the store's data format (log2 F rounded
+    to fp32, include/orloj.h orloj_store) instead of exactly."""
+    c = np.asarray(counts, dtype=np.float64)
+    F = np.cumsum(c, axis=1) / c.sum(axis=1, keepdims=True)
+    if store_fp32:
+        with np.errstate(divide="ignore"):
+            F = np.exp2(np.log2(F).astype(np.float32).astype(np.float64))
+    wts = np.ones(c.shape[0]) if weights is None else np.asarray(weights, dtype=np.float64)
+    return (wts[:, None] * F).sum(axis=0) / wts.sum()
+
+
+def batch_latency_pmf(counts, bs, weights=None, store_fp32=False) -> np.ndarray:
+    """pm_i = P(L_bs in bin i), i = 1..B: the max of bs i.i.d. mixture draws
+    (Eq. 6 with identical factors): F_mix^bs differenced."""
+    G = mixture_cdf(counts, weights, store_fp32) ** bs
+    G[-1] = 1.0
+    return np.diff(np.concatenate([[0.0], G]))
+
+
+def expected_latency(pm, a, w) -> float:
+    """E[L] of the histogram with uniform bins (l1, l2]: sum pm_i (l1 + l2)/2."""
+    i = np.arange(1, len(pm) + 1, dtype=np.float64)
+    return float(np.sum(pm * (a + w * (i - 0.5))))
+
+
+def log_priority(pm, a, w, b, sigma) -> np.ndarray:
+    """log p for slacks sigma = D - t (array), Eq. 2 bin by bin:
+         t <  D - l2:        (h/(E[L] b)) (e^{b l2} - e^{b l1}) e^{-b D} e^{b t}
+         D - l2 <= t < D - l1: h/(E[L] b) - (h/(E[L] b)) e^{b l1} e^{-b D} e^{b t}
+         D - l1 <= t:        0
+       with c = 1 and h = pm_i / w, combined p = sum_i p_i.  Each term is
+       evaluated as its logarithm (e^{b l2} e^{-bD} e^{bt} = e^{-b(sigma - l2)})
+       and the sum by logaddexp, so no term overflows."""
+    pm = np.asarray(pm, dtype=np.float64)
+    sig = np.atleast_1d(np.asarray(sigma, dtype=np.float64))
+    EL = expected_latency(pm, a, w)
+    out = np.full(sig.shape, -np.inf)
+    for i in range(1, len(pm) + 1):
+        if pm[i - 1] <= 0.0:
+            continue
+        l1, l2 = a + w * (i - 1), a + w * i
+        logh_b = np.log(pm[i - 1] / w / b)
+        term = np.full(sig.shape, -np.inf)
+        full = sig >= l2
+        part = (sig > l1) & (sig < l2)
+        # (e^{b l2} - e^{b l1}) e^{-b sigma} = e^{-b (sigma - l2)} (1 - e^{-b w})
+        term[full] = logh_b - b * (sig[full] - l2) + np.log1p(-np.exp(-b * w))
+        # 1 - e^{b l1} e^{-b sigma} = 1 - e^{-b (sigma - l1)}
+        term[part] = logh_b + np.log1p(-np.exp(-b * (sig[part] - l1)))
+        out = np.logaddexp(out, term)
+    return out - np.log(EL)
+
+
+def scores(counts, a, w, num_sizes, b, offsets, deadline, now, weights=None, store_fp32=False) -> np.ndarray:
+    """log p [N][num_sizes] for queue members (offsets relative to offsets[0]),
+    slack D_r - now[q]; a, w are the profile arrays (index bs-1)."""
+    off = np.asarray(offsets, dtype=np.int64) - int(offsets[0])
+    dl = np.asarray(deadline, dtype=np.int64)
+    out = np.empty((int(off[-1]), num_sizes))
+    sig = np.empty(int(off[-1]), dtype=np.int64)
+    for q in range(len(off) - 1):
+        sig[off[q]:off[q + 1]] = dl[off[q]:off[q + 1]] - int(now[q])
+    for bs in range(1, num_sizes + 1):
+        pm = batch_latency_pmf(counts, bs, weights, store_fp32)
+        out[:, bs - 1] = log_priority(pm, float(a[bs - 1]), float(w[bs - 1]), b, sig)
+    return out
+
+
+def pop_batch(logp_rows, bs, num_sizes, cap=256) -> list[int]:
+    """PopBatch (Alg. 1 line 18): the (up to) bs members with the highest
+    priority for size bs, highest first, ties to the earlier member, members
+    with p = 0 (log p = -inf) or NaN never selected; only the first `cap`
+    members are candidates (the ABI's window)."""
+    if not (1 <= bs <= num_sizes):
+        return []
+    cand = [(-float(v), r) for r, v in enumerate(logp_rows[:cap, bs - 1])
+            if not (np.isnan(v) or v == -np.inf)]
+    return [r for _, r in sorted(cand)[:bs]]

@@ -234,6 +234,49 @@ def pick_batch(store: HistogramStore, profile: LatencyProfile, queues: Queues, b
     return best_k, best_E
 
 
+class PriorityTable:
+    """Eq. 1-2 priorities for batch sizes 1..num_sizes, with
+    the batch-latency distribution of each size from the mixture of all
+    applications, precomputed off the critical path
+    (orloj_priority_table); `scores` evaluates log p for every queue member and
+    size, `pop` selects the top members of a size per queue (PopBatch)."""
+
+    def __init__(self, store: HistogramStore, profile: LatencyProfile, num_sizes: int, b_per_tick: float,
+                 weights: Optional[torch.Tensor] = None, stream=None):
+        dev = store.log2_cdf.device
+        self.store, self.profile = store, profile
+        self.S, self.b = int(num_sizes), float(b_per_tick)
+        self.log_table = torch.empty((self.S, 2, store.num_bins + 1), dtype=torch.float64, device=dev)
+        self.log_expected = torch.empty(self.S, dtype=torch.float64, device=dev)
+        if weights is not None:
+            _dev(weights, torch.float32, "weights")
+        _abi.check(_abi.lib().orloj_priority_table(store.c(), profile.c(), self.S, _ptr(weights), self.b,
+                                                   self.log_table.data_ptr(), self.log_expected.data_ptr(),
+                                                   _stream_ptr(stream)))
+
+    def scores(self, queues: Queues, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        N = queues.deadline.numel()
+        if out is None:
+            out = torch.empty((self.S, N), dtype=torch.float32, device=queues.now.device)
+        _abi.check(_abi.lib().orloj_priority_scores(self.store.c(), self.profile.c(), self.S, self.b,
+                                                    self.log_table.data_ptr(), self.log_expected.data_ptr(),
+                                                    queues.c(), _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def pop(self, queues: Queues, log_priority: torch.Tensor, batch_size: torch.Tensor, stream=None,
+            out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Selected member indices [Q][32] (-1 padded) for the [S][N] scores."""
+        _dev(log_priority, torch.float32, "log_priority")
+        _dev(batch_size, torch.int32, "batch_size")
+        if log_priority.dim() != 2 or log_priority.shape[0] != self.S:
+            raise OrlojError(1, "log_priority must be [num_sizes, N]")
+        sel = out if out is not None else torch.empty((queues.num_queues, 32), dtype=torch.int32,
+                                                      device=queues.now.device)
+        _abi.check(_abi.lib().orloj_pop_batch(queues.c(), log_priority.data_ptr(), self.S, batch_size.data_ptr(),
+                                              _ptr(sel), _stream_ptr(stream)))
+        return sel
+
+
 class HostPicker:
     """End-to-end pick for queues in pinned host memory (orloj_pick_batch_host).
 

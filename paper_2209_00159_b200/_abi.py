@@ -83,6 +83,11 @@ SIGNATURES = {
                                           ctypes.POINTER(TraceC), _P, _P, _P]),
     "orloj_replay_trace_ex": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
                                              ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC), _P, _P, _P]),
+    "orloj_priority_table": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,
+                                            _P, ctypes.c_double, _P, _P, _P]),
+    "orloj_priority_scores": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,
+                                             ctypes.c_double, _P, _P, ctypes.POINTER(QueuesC), _P, _P]),
+    "orloj_pop_batch": (ctypes.c_int, [ctypes.POINTER(QueuesC), _P, ctypes.c_int32, _P, _P, _P]),
     "orloj_histogram_accumulate": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int32,
                                                   ctypes.c_int32, _P]),
     "orloj_validate_store": (ctypes.c_int, [ctypes.POINTER(Store), _P]),

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "replay_kernel.cuh"
 #include "score_kernel.cuh"
+#include "priority_kernel.cuh"
 #include "store_kernel.cuh"
 
 using namespace orloj;
@@ -162,6 +163,18 @@ cudaError_t launch_score(const ScoreParams &p, bool pick, int64_t store_bytes, c
                      : store_bytes > STREAM_STORE_BYTES ? RowSrc::TmaStream
                                                         : RowSrc::Tma;
   return pick ? launch_score_b<true>(p, src, s) : launch_score_b<false>(p, src, s);
+}
+
+template <bool SMEM_TABLE>
+cudaError_t prio_attr() {
+  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
+  if (!configured.load(std::memory_order_acquire)) {
+    const cudaError_t e = cudaFuncSetAttribute(priority_scores_kernel<SMEM_TABLE>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_release);
+  }
+  return cudaSuccess;
 }
 
 orloj_status prepare_score(const orloj_store *store, const orloj_latency_profile *profile,
@@ -367,6 +380,78 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_trace launch");
+  return ok();
+}
+
+orloj_status orloj_priority_table(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
+                                  const float *weights, double b, double *log_table, double *log_expected,
+                                  void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
+  ProfileDev prof;
+  if ((st = compile_profile(profile, store->num_bins, ORLOJ_MAX_KMAX, &prof))) return st;
+  if (S < 1 || S > profile->kmax || !(b > 0.0) || !log_table || !log_expected)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_table: need 1 <= num_sizes <= kmax, b > 0, outputs");
+  for (int k = 0; k < S; ++k)
+    if (!(b * prof.w[k] < 700.0)) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_table: b * w_%d >= 700", k + 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  priority_table_kernel<<<S, 128, (size_t)store->num_bins * 8, s>>>(store->log2_cdf, store->num_dists,
+                                                                     store->num_bins, weights, prof, b, log_table,
+                                                                     log_expected);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "priority_table");
+  return ok();
+}
+
+orloj_status orloj_priority_scores(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
+                                   double b, const double *log_table, const double *log_expected,
+                                   const orloj_queues *queues, float *out, void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
+  if ((st = check_queues(queues))) return st;
+  ProfileDev prof;
+  if ((st = compile_profile(profile, store->num_bins, ORLOJ_MAX_KMAX, &prof))) return st;
+  if (S < 1 || S > profile->kmax || !(b > 0.0) || !log_table || !log_expected)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores: need 1 <= num_sizes <= kmax, b > 0, tables");
+  if (queues->num_queues == 0) return ok();
+  if (!out) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores: output is NULL");
+  // Grid-stride over queues: ~resident blocks, so the per-size constants are
+  // staged once per block, not once per 8 queues.
+  const int B = store->num_bins;
+  const bool smem_table = PrioSmem::table_bytes(S, B) <= (64u << 10);
+  const size_t smem = PrioSmem::bytes(S, B, smem_table);
+  cudaError_t e = smem_table ? prio_attr<true>() : prio_attr<false>();
+  if (e != cudaSuccess) return cuda_fail(e, "priority_scores attributes");
+  const int64_t want = (queues->num_queues + 7) / 8;
+  const int per_sm = smem <= (24u << 10) ? 8 : (int)((200u << 10) / smem);
+  const int64_t cap = (int64_t)148 * (per_sm < 1 ? 1 : per_sm);
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  if (smem_table)
+    priority_scores_kernel<true><<<grid, 256, smem, (cudaStream_t)stream>>>(
+        log_table, log_expected, S, B, b, prof, queues->num_queues, queues->queue_offsets, queues->deadline_ticks,
+        queues->now_ticks, out);
+  else
+    priority_scores_kernel<false><<<grid, 256, smem, (cudaStream_t)stream>>>(
+        log_table, log_expected, S, B, b, prof, queues->num_queues, queues->queue_offsets, queues->deadline_ticks,
+        queues->now_ticks, out);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "priority_scores launch");
+  return ok();
+}
+
+orloj_status orloj_pop_batch(const orloj_queues *queues, const float *logp, int32_t S, const int32_t *bs,
+                             int32_t *sel, void *stream) {
+  orloj_status st;
+  if ((st = check_queues(queues))) return st;
+  if (S < 1) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pop_batch: num_sizes < 1");
+  if (queues->num_queues == 0) return ok();
+  if (!logp || !bs || !sel) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pop_batch: NULL array");
+  const int64_t threads = queues->num_queues * 32;
+  pop_batch_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      logp, S, queues->num_queues, queues->queue_offsets, bs, sel);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "pop_batch launch");
   return ok();
 }
 

@@ -1,0 +1,180 @@
+"""GPU parity: Eq. 1-2 priority scores and PopBatch (orloj_priority_table /
+orloj_priority_scores / orloj_pop_batch) vs oracle/priority.py.
+
+Tolerance on log p (R10-R12): the CUDA path reads the store,
+whose data format is log2 F rounded to fp32 (include/orloj.h), and writes
+fp32 log p.  The oracle reads the same format (oracle.priority
+store_fp32=True: counts -> fp64 log2 F -> fp32, its own arithmetic).  The
+tables are fp64 (error < 1e-9 after the bin-mass cancellation G_i - G_{i-1});
+per element the full-bin term C[i*] - b sigma - log E[L] is formed in fp64 and
+rounded once to fp32 (2^-24 relative), the partial-bin term is fp32 (its
+log(h/b) - log E[L] rounded once, 1 - e^{-bx} by expm1f, <= 2 ulp), and the
+log-add-exp (log1pf(exp(d)) in [0, ln 2], abs error < 2^-22) plus the final
+add (2^-24 relative): |d log p| <= 1e-6 + 2^-22 |log p| (each term's relative
+error enters with its softmax weight, so never more than the larger term's
+share).  (The fp32
+store itself moves a bin mass pm_i by up to bs 2^-25 |log2 F| ln2 G_i / pm_i
+relative, large for near-empty bins at large bs: a property of the store
+format, not of these kernels.)
+-inf (p = 0: no outcome of L_bs fits before the deadline) must match exactly.
+PopBatch is integer work: bit-exact against the oracle on the same fp32
+scores (seeded inputs, not GPU outputs).
+"""
+import numpy as np
+import pytest
+
+import gen
+from oracle import priority as pr
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2209_00159_b200 as orj  # noqa: E402
+import workloads as wl  # noqa: E402
+
+S = 32
+
+
+def _tol(ref):
+    return 1e-6 + 2.0 ** -22 * np.abs(ref)
+
+
+def _case(name, seed, Q=96):
+    fam = {"skipnet": gen.skipnet_family, "rdi": gen.rdi_family, "gpt": gen.gpt_family}[name](seed)
+    prof = gen.eq3_half(fam, S)
+    rng = np.random.default_rng(seed + 7)
+    lengths = rng.integers(0, 300, Q)
+    lengths[:3] = (0, 1, 256)
+    q = gen.snapshot_queues(seed, lengths, fam.p99_ticks(), D=fam.D)
+    # a few queues observed after their deadlines (negative slack)
+    q.now[4:8] += 3 * fam.p99_ticks()
+    return fam, prof, q
+
+
+def _gpu_scores(fam, prof, q, b, weights=None):
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    p = orj.LatencyProfile(prof.a, prof.w)
+    wt = None if weights is None else torch.tensor(weights, dtype=torch.float32, device="cuda")
+    tab = orj.PriorityTable(store, p, S, b, weights=wt)
+    qs = wl.device_queues(q)
+    lp = tab.scores(qs)
+    torch.cuda.synchronize()
+    return tab, qs, lp
+
+
+@pytest.mark.parametrize("name", ["skipnet", "rdi", "gpt"])
+@pytest.mark.parametrize("b_scale", [0.05, 1.0, 20.0])
+def test_scores_vs_oracle(name, b_scale):
+    fam, prof, q = _case(name, gen.SEED_BASE + 910)
+    b = b_scale / fam.mean_ticks()  # anticipated delay ~ mean latency / b_scale
+    weights = None if b_scale != 1.0 else np.linspace(0.5, 2.0, fam.D)
+    _, _, lp = _gpu_scores(fam, prof, q, b, weights)
+    got = lp.cpu().numpy().T.astype(np.float64)
+    ref = pr.scores(fam.counts, prof.a, prof.w, S, b, q.offsets, q.deadline, q.now, weights, store_fp32=True)
+    assert got.shape == ref.shape
+    ninf = ref == -np.inf
+    assert (np.isneginf(got) == ninf).all(), int((np.isneginf(got) != ninf).sum())
+    err = np.abs(got[~ninf] - ref[~ninf])
+    assert (err <= _tol(ref[~ninf])).all(), float(err.max())
+    exact = pr.scores(fam.counts, prof.a, prof.w, S, b, q.offsets, q.deadline, q.now, weights)
+    assert ((exact == -np.inf) == ninf).all()
+
+
+def test_scores_queue_window_and_empty():
+    fam, prof, q = _case("gpt", gen.SEED_BASE + 911, Q=24)
+    b = 1.0 / fam.mean_ticks()
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    p = orj.LatencyProfile(prof.a, prof.w)
+    tab = orj.PriorityTable(store, p, S, b)
+    full = wl.device_queues(q)
+    lp_full = tab.scores(full)
+    # queues 5..16 through offsets that start at member offsets[5]
+    o0, o1 = int(q.offsets[5]), int(q.offsets[17])
+    sub = orj.Queues(full.offsets[5:18].contiguous(), full.deadline[o0:o1].contiguous(),
+                     full.dist[o0:o1].contiguous(), full.now[5:17].contiguous())
+    lp_sub = tab.scores(sub)
+    torch.cuda.synchronize()
+    assert torch.equal(lp_sub, lp_full[:, o0:o1])
+    empty = orj.Queues.from_numpy(np.zeros(1, np.int64), np.zeros(0), np.zeros(0), np.zeros(0))
+    assert tab.scores(empty).numel() == 0
+
+
+def test_table_properties():
+    fam, prof, _ = _case("rdi", gen.SEED_BASE + 912)
+    b = 1.0 / fam.mean_ticks()
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    tab = orj.PriorityTable(store, orj.LatencyProfile(prof.a, prof.w), S, b)
+    torch.cuda.synchronize()
+    EL = np.exp(tab.log_expected.cpu().numpy())
+    ref = np.array([pr.expected_latency(pr.batch_latency_pmf(fam.counts, bs, store_fp32=True), prof.a[bs - 1],
+                                        prof.w[bs - 1])
+                    for bs in range(1, S + 1)])
+    assert np.allclose(EL, ref, rtol=1e-12, atol=0)
+    C = tab.log_table[:, 0].cpu().numpy()
+    assert (C[:, 1:] >= C[:, :-1]).all()  # prefix of non-negative terms
+    assert (C[:, 0] == -np.inf).all() and np.isfinite(C[:, -1]).all()
+
+
+def test_invalid_arguments():
+    fam, prof, _ = _case("gpt", gen.SEED_BASE + 913)
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    p = orj.LatencyProfile(prof.a, prof.w)
+    for bad in (dict(num_sizes=0, b_per_tick=1e-3), dict(num_sizes=S + 1, b_per_tick=1e-3),
+                dict(num_sizes=4, b_per_tick=0.0), dict(num_sizes=4, b_per_tick=1e9)):
+        with pytest.raises(orj.OrlojError):
+            orj.PriorityTable(store, p, **bad)
+
+
+def _pop_case(seed, Q=300):
+    rng = np.random.default_rng(seed)
+    lengths = rng.integers(0, 320, Q)
+    lengths[:4] = (0, 1, 256, 319)
+    off = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    N = int(off[-1])
+    v = rng.integers(-40, 40, size=(N, S)).astype(np.float32) * np.float32(0.25)  # many exact ties
+    v[rng.random((N, S)) < 0.2] = -np.inf
+    v[rng.random((N, S)) < 0.02] = np.nan
+    v[rng.random((N, S)) < 0.05] = np.float32(-0.0)
+    bs = rng.integers(-1, S + 3, Q).astype(np.int32)
+    bs[:8] = (1, 32, 32, 32, 0, S + 1, 5, 17)
+    return off, v, bs
+
+
+def test_pop_batch_bitexact():
+    off, v, bs = _pop_case(gen.SEED_BASE + 914)
+    Q = len(bs)
+    q = orj.Queues.from_numpy(off, np.zeros(off[-1]), np.zeros(off[-1]), np.zeros(Q))
+    fam = gen.gpt_family(gen.SEED_BASE + 915)
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    prof = gen.eq3_half(fam, S)
+    tab = orj.PriorityTable(store, orj.LatencyProfile(prof.a, prof.w), S, 1e-4)
+    sel = tab.pop(q, torch.from_numpy(np.ascontiguousarray(v.T)).cuda(), torch.from_numpy(bs).cuda()).cpu().numpy()
+    for qi in range(Q):
+        want = pr.pop_batch(v[off[qi]:off[qi + 1]], int(bs[qi]), S)
+        got = [int(x) for x in sel[qi] if x >= 0]
+        assert got == want, qi
+        assert (sel[qi, len(got):] == -1).all()
+
+
+def test_scores_then_pop_selects_the_top():
+    """End to end: GPU scores -> GPU PopBatch selects members whose oracle
+    priority is within the score tolerance of the oracle's top-bs (several
+    selections are correct under ties, A9-style: compare the unique part)."""
+    fam, prof, q = _case("skipnet", gen.SEED_BASE + 916)
+    b = 1.0 / fam.mean_ticks()
+    tab, qs, lp = _gpu_scores(fam, prof, q, b)
+    rng = np.random.default_rng(gen.SEED_BASE + 917)
+    bs = rng.integers(1, S + 1, q.Q).astype(np.int32)
+    sel = tab.pop(qs, lp, torch.from_numpy(bs).cuda()).cpu().numpy()
+    ref = pr.scores(fam.counts, prof.a, prof.w, S, b, q.offsets, q.deadline, q.now, store_fp32=True)
+    for qi in range(q.Q):
+        rows = ref[q.offsets[qi]:q.offsets[qi + 1], bs[qi] - 1][:256]
+        want = pr.pop_batch(ref[q.offsets[qi]:q.offsets[qi + 1]], int(bs[qi]), S)
+        got = [int(x) for x in sel[qi] if x >= 0]
+        assert len(got) == len(want)
+        if want:
+            kth = rows[want[-1]]
+            assert all(rows[r] >= kth - 2 * _tol(kth) for r in got)

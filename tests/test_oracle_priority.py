@@ -1,0 +1,154 @@
+"""Pins of oracle/priority.py (Eq. 1-2 priority, batch latency of a mixture,
+PopBatch) against what the paper and the mathematics fix, independent of the
+oracle's own formulas:
+
+* the batch-latency pmf against brute-force enumeration of every bs-tuple of
+  (application, bin) draws (Eq. 6 with a mixture);
+* log p against Eq. 1 evaluated from its DEFINITION, p = (E[C_delay] -
+  E[C_now]) / E[L] with C = 1[t > D], tau ~ Exp(b): by numerical
+  quadrature of the convolution P(tau + L <= sigma) and by Monte Carlo;
+* E[L] against the quadrature of the survival function;
+* the limits b -> 0 (p -> P(L <= sigma) / E[L]) and the milestone form
+  p(t) = alpha e^{bt} + beta between milestones;
+* PopBatch against the order invariants of "the bs highest priorities".
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+from scipy import integrate
+
+import gen
+from oracle import priority as pr
+
+
+def _fam():
+    rng = np.random.default_rng(gen.SEED_BASE + 901)
+    D, B = 3, 6
+    counts = rng.integers(0, 9, size=(D, B))
+    counts[:, 2] += 1  # every row has a positive total
+    return counts
+
+
+def _F_L(pm, a, w):
+    """Piecewise-linear CDF of L with pm spread uniformly over (a + w(i-1), a + w i]."""
+    edges = a + w * np.arange(len(pm) + 1, dtype=np.float64)
+    G = np.concatenate([[0.0], np.cumsum(pm)])
+    return lambda x: float(np.interp(x, edges, G, left=0.0, right=1.0)), edges
+
+
+@pytest.mark.parametrize("bs", [1, 2, 3])
+def test_batch_pmf_bruteforce(bs):
+    counts = _fam()
+    D, B = counts.shape
+    wts = np.array([1.0, 2.0, 0.5])
+    p_draw = (wts[:, None] * counts / counts.sum(axis=1, keepdims=True)) / wts.sum()  # P(app d, bin i)
+    pm = np.zeros(B)
+    cells = [(d, i) for d in range(D) for i in range(B)]
+    for tup in itertools.product(cells, repeat=bs):
+        pm[max(i for _, i in tup)] += math.prod(p_draw[d, i] for d, i in tup)
+    got = pr.batch_latency_pmf(counts, bs, wts)
+    assert np.allclose(got, pm, rtol=0, atol=1e-14)
+    assert abs(got.sum() - 1.0) < 1e-14
+
+
+@pytest.mark.parametrize("bs,b", [(1, 1e-3), (2, 2e-2), (3, 3e-4)])
+def test_priority_matches_eq1_definition_quadrature(bs, b):
+    counts = _fam()
+    a, w = 250.0, 100.0
+    pm = pr.batch_latency_pmf(counts, bs)
+    F, edges = _F_L(pm, a, w)
+    EL_quad = integrate.quad(lambda x: 1.0 - F(x), 0.0, edges[-1], points=list(edges), limit=200)[0]
+    assert abs(pr.expected_latency(pm, a, w) - EL_quad) < 1e-9 * EL_quad
+    sig = np.array([-50.0, 0.0, a - 1, a, a + 37.0, a + w, a + 2.5 * w, a + 4 * w + 1, edges[-1], edges[-1] + 300.0])
+    got = pr.log_priority(pm, a, w, b, sig)
+    for s, lp in zip(sig, got):
+        # E[C_delay] - E[C_now] = P(t + tau + L > D) - P(t + L > D) = F_L(sigma) - P(tau + L <= sigma)
+        if s <= 0:
+            conv = 0.0
+        else:
+            pts = [s - e for e in edges if 0 < s - e < s]
+            conv = integrate.quad(lambda u: b * math.exp(-b * u) * F(s - u), 0.0, s, points=pts or None,
+                                  limit=400, epsabs=1e-15, epsrel=1e-12)[0]
+        p_def = (F(s) - conv) / EL_quad
+        if p_def <= 1e-300:
+            assert lp == -np.inf
+        else:
+            assert abs(math.exp(lp) - p_def) <= 1e-9 * p_def + 1e-15, (s, math.exp(lp), p_def)
+
+
+def test_priority_monte_carlo():
+    counts = _fam()
+    a, w, b, bs = 250.0, 100.0, 4e-3, 2
+    pm = pr.batch_latency_pmf(counts, bs)
+    rng = np.random.default_rng(gen.SEED_BASE + 902)
+    n = 2_000_000
+    i = rng.choice(len(pm), size=n, p=pm / pm.sum())
+    L = a + w * (i + rng.random(n))
+    tau = rng.exponential(1.0 / b, size=n)
+    EL = L.mean()
+    for s in (a + 1.5 * w, a + 3.2 * w, a + 7 * w):
+        x = ((L <= s) & (tau + L > s)).astype(np.float64)
+        est, se = x.mean() / EL, x.std() / math.sqrt(n) / EL
+        p = math.exp(pr.log_priority(pm, a, w, b, [s])[0])
+        assert abs(p - est) <= 5 * se + 1e-4 * p
+
+
+def test_small_b_limit_and_milestone_form():
+    counts = _fam()
+    a, w, bs = 250.0, 100.0, 3
+    pm = pr.batch_latency_pmf(counts, bs)
+    F, edges = _F_L(pm, a, w)
+    EL = pr.expected_latency(pm, a, w)
+    b = 1e-10
+    for s in (a + 0.5 * w, a + 2 * w, edges[-1] + 10):
+        p = math.exp(pr.log_priority(pm, a, w, b, [s])[0])
+        # b -> 0: tau -> infinity, E[C_delay] -> 1, p -> F_L(sigma) / E[L]
+        assert abs(p - F(s) / EL) <= 1e-6 * F(s) / EL
+    # beyond the last milestone (sigma >= a + wB) only full bins remain:
+    # p(t) = alpha e^{bt}, i.e. p(sigma + d) = p(sigma) e^{-bd}
+    b = 2e-3
+    s0 = edges[-1] + 5
+    l0, l1 = pr.log_priority(pm, a, w, b, [s0, s0 + 321.0])
+    assert abs((l1 - l0) + b * 321.0) < 1e-12
+    # between two milestones inside bin i the form is alpha e^{bt} + beta: second
+    # differences of p in t obey p'' = b p' (no other terms)
+    s = a + 2 * w + np.array([20.0, 40.0, 60.0])
+    p = np.exp(pr.log_priority(pm, a, w, b, s))
+    # t = D - sigma: in t, p = alpha e^{bt} + beta with equally spaced t -> geometric differences
+    d1, d2 = p[1] - p[0], p[2] - p[1]
+    assert abs(d1 / d2 - math.exp(b * 20.0)) < 1e-9
+
+
+def test_priority_zero_before_any_outcome():
+    counts = _fam()
+    counts[:, :2] = 0
+    pm = pr.batch_latency_pmf(counts, 2)
+    a, w = 100.0, 50.0
+    got = pr.log_priority(pm, a, w, 1e-3, [a + 2 * w, a + 2 * w + 1])
+    assert got[0] == -np.inf and np.isfinite(got[1])
+
+
+def test_pop_batch_invariants():
+    rng = np.random.default_rng(gen.SEED_BASE + 903)
+    for trial in range(200):
+        n, S = int(rng.integers(0, 300)), 4
+        v = rng.integers(-5, 5, size=(n, S)).astype(np.float32)
+        v[rng.random((n, S)) < 0.15] = -np.inf
+        v[rng.random((n, S)) < 0.05] = np.nan
+        bs = int(rng.integers(0, 6))
+        sel = pr.pop_batch(v, bs, S)
+        if not 1 <= bs <= S:
+            assert sel == []
+            continue
+        col = v[:256, bs - 1]
+        ok = [r for r in range(len(col)) if np.isfinite(col[r])]
+        assert len(sel) == min(bs, len(ok)) and len(set(sel)) == len(sel)
+        assert all(r in ok for r in sel)
+        rest = [r for r in ok if r not in sel]
+        for j, r in enumerate(sel):
+            if j:
+                assert (col[sel[j - 1]], -sel[j - 1]) > (col[r], -r)
+            for u in rest:  # every unselected candidate is lower, or equal and later
+                assert (col[r], -r) > (col[u], -u)
