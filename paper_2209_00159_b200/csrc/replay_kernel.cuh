@@ -134,7 +134,77 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   long long c_fin = 0, c_drop = 0, c_late = 0, c_bat = 0, c_busy = 0;
   int64_t ndec = 0;
 
+  // consume m (< 32) arrivals from the lookahead: shift by m lanes, refill the
+  // tail from HBM (used from the next decision on)
+  auto advance = [&](int m) {
+    cursor += m;
+    const int src = (lane + m) & 31;
+    const int64_t sa = __shfl_sync(FULL, ua, src);
+    const int sd = __shfl_sync(FULL, ud, src);
+    const int st = __shfl_sync(FULL, ut, src);
+    if (lane + m < 32) {
+      ua = sa;
+      ud = sd;
+      ut = st;
+    } else {
+      const int64_t idx = cursor + lane;
+      ua = INT64_MAX;
+      if (idx < n) {
+        ua = arr[idx];
+        ud = dis[idx];
+        ut = tbs[idx];
+      }
+    }
+  };
+  const int64_t a1 = p.prof.a[0], w1 = p.prof.w[0];
+
   while (cursor < n || ncarry > 0) {
+    // ---- 0. runs of single-member windows (max-plus scan) -----------------
+    // With nothing carried, arrival j of the lookahead is a window of one iff
+    // it is not hopeless at its decision time t'_j = max(T_{j-1}, a_j) and the
+    // next arrival comes later (a_{j+1} > t'_j); its batch then ends at
+    // T_j = t'_j + d_j, d_j = a_1 + w_1 bin_j.  T_j = g_j(T_{j-1}) with
+    // g_j(x) = max(x + d_j, a_j + d_j): maps (P, Q): x -> max(x + P, Q) compose
+    // associatively, (P, Q) then (P', Q') = (P + P', max(Q + P', Q')), so a
+    // warp scan yields up to 31 consecutive decisions at once; the leading run
+    // of lanes meeting both conditions is committed, exactly as the sequential
+    // loop would (window of one: k* = 1, no scoring).
+    if (ncarry == 0) {
+      const bool va = ua != INT64_MAX;
+      const int64_t dj = a1 + w1 * ut;
+      const int64_t hj = va ? ua + slo - s_thr[ud] : INT64_MIN;
+      const int64_t an = __shfl_down_sync(FULL, ua, 1);
+      const int64_t t0 = __shfl_sync(FULL, ua, 0) > t ? __shfl_sync(FULL, ua, 0) : t;
+      const bool ok0 = __shfl_sync(FULL, an, 0) > t0 && t0 <= __shfl_sync(FULL, hj, 0) &&
+                       __shfl_sync(FULL, (int)va, 0);
+      if (ok0) {  // warp-uniform
+        int64_t P = va ? dj : 0, Qv = va ? ua + dj : INT64_MIN;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int64_t Pp = __shfl_up_sync(FULL, P, off);
+          const int64_t Qp = __shfl_up_sync(FULL, Qv, off);
+          if (lane >= off) {
+            const int64_t q2 = Qp + P;
+            Qv = q2 > Qv ? q2 : Qv;
+            P += Pp;
+          }
+        }
+        const int64_t Tj = t + P > Qv ? t + P : Qv;  // t may be INT64_MIN: t + P does not overflow
+        const int64_t tpj = Tj - dj;
+        const bool ok = lane < 31 && va && an > tpj && tpj <= hj;
+        const int m = __ffs(~__ballot_sync(FULL, ok)) - 1;  // >= 1 (lane 0 passed ok0)
+        const unsigned fm = __ballot_sync(FULL, lane < m && Tj <= ua + slo);
+        c_fin += __popc(fm);
+        c_late += m - __popc(fm);
+        c_bat += m;
+        c_busy += __shfl_sync(FULL, P, m - 1);
+        t = __shfl_sync(FULL, Tj, m - 1);
+        if (p.log && lane < m) p.log[base + s + ndec + lane] = 1;
+        ndec += m;
+        advance(m);
+        continue;
+      }
+    }
     const int64_t next_arr = __shfl_sync(FULL, ua, 0);
     if (ncarry == 0 && next_arr > t) t = next_arr;  // idle worker: jump to the next arrival (A15)
     // ---- 1. scan -------------------------------------------------------
@@ -190,17 +260,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       }
       wc += __popc(kc);
       const int nc = __popc(consumed);
-      cursor += nc;
-      // shift the lookahead by nc lanes; refill its tail from HBM (used next decision)
-      const int src = (lane + nc) & 31;
-      const int64_t sa = __shfl_sync(FULL, ua, src);
-      const int sd = __shfl_sync(FULL, ud, src);
-      const int st = __shfl_sync(FULL, ut, src);
-      if (lane + nc < 32) {
-        ua = sa;
-        ud = sd;
-        ut = st;
-      } else {
+      if (nc == 32) {  // whole lookahead consumed: reload all of it, scan on
+        cursor += 32;
         const int64_t idx = cursor + lane;
         ua = INT64_MAX;
         if (idx < n) {
@@ -208,8 +269,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
           ud = dis[idx];
           ut = tbs[idx];
         }
+        continue;
       }
-      if (nc < 32) break;
+      advance(nc);
+      break;
     }
     ncarry = 0;
     carry_off = 0;
