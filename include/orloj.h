@@ -271,6 +271,24 @@ orloj_status orloj_priority_scores(const orloj_store *store, const orloj_latency
                                    int32_t num_sizes, double b_per_tick, const double *log_table,
                                    const double *log_expected, const orloj_queues *queues, float *log_priority,
                                    void *stream);
+/* Piecewise-step cost: a request misses deadline D_r + offset[s]
+ * at cumulative cost cost[s]; the cost function decomposes into single steps at
+ * D_r + offset[s] with cost cost[s] - cost[s-1] (cost[-1] = 0), and the
+ * priority is the sum of the single-step priorities (Eq. 2 each, same E[L]).
+ * offset_ticks: host int64 [num_steps], strictly increasing, |offset| <= 2^40;
+ * cost: host double [num_steps], strictly increasing from > 0; 1 <= num_steps
+ * <= 8.  Copied at the call (no ownership kept). */
+typedef struct {
+  int32_t num_steps;
+  const int64_t *offset_ticks;
+  const double *cost;
+} orloj_cost_steps;
+/* orloj_priority_scores with a piecewise-step cost per request (same layout);
+ * steps = {1, {0}, {1.0}} reproduces orloj_priority_scores.  Async. */
+orloj_status orloj_priority_scores_steps(const orloj_store *store, const orloj_latency_profile *profile,
+                                         int32_t num_sizes, double b_per_tick, const double *log_table,
+                                         const double *log_expected, const orloj_queues *queues,
+                                         const orloj_cost_steps *steps, float *log_priority, void *stream);
 /* PopBatch: per queue q, the (up to) batch_size[q] <= 32 members with the
  * highest log p for that size (ties -> earlier member; -inf and NaN never
  * chosen), among the first 256 members; log_priority is the [num_sizes][N]

@@ -37,12 +37,26 @@ def mixture_cdf(counts, weights=None, store_fp32=False) -> np.ndarray:
     return (wts[:, None] * F).sum(axis=0) / wts.sum()
 
 
+def batch_latency_logpmf(counts, bs, weights=None, store_fp32=False) -> np.ndarray:
+    """log pm_i, pm_i = P(L_bs in bin i), i = 1..B: the max of bs i.i.d. mixture
+    draws (Eq. 6 with identical factors), G = F_mix^bs differenced.  Evaluated
+    as log G_i = bs log F_mix and log(G_i - G_{i-1}) = log G_i +
+    log(1 - exp(log G_{i-1} - log G_i)), the same quantity without the fp64
+    underflow of F^bs for small F and large bs."""
+    F = mixture_cdf(counts, weights, store_fp32)
+    F[-1] = 1.0
+    with np.errstate(divide="ignore"):
+        lG = bs * np.log(F)
+    prev = np.concatenate([[-np.inf], lG[:-1]])
+    out = np.full(lG.shape, -np.inf)
+    pos = lG > prev
+    out[pos] = lG[pos] + np.log(-np.expm1(prev[pos] - lG[pos]))
+    return out
+
+
 def batch_latency_pmf(counts, bs, weights=None, store_fp32=False) -> np.ndarray:
-    """pm_i = P(L_bs in bin i), i = 1..B: the max of bs i.i.d. mixture draws
-    (Eq. 6 with identical factors): F_mix^bs differenced."""
-    G = mixture_cdf(counts, weights, store_fp32) ** bs
-    G[-1] = 1.0
-    return np.diff(np.concatenate([[0.0], G]))
+    """pm_i = P(L_bs in bin i), i = 1..B (linear; see batch_latency_logpmf)."""
+    return np.exp(batch_latency_logpmf(counts, bs, weights, store_fp32))
 
 
 def expected_latency(pm, a, w) -> float:
@@ -52,6 +66,12 @@ def expected_latency(pm, a, w) -> float:
 
 
 def log_priority(pm, a, w, b, sigma) -> np.ndarray:
+    """log p from the bin masses pm (see log_priority_lp)."""
+    with np.errstate(divide="ignore"):
+        return log_priority_lp(np.log(np.asarray(pm, dtype=np.float64)), a, w, b, sigma)
+
+
+def log_priority_lp(lpm, a, w, b, sigma) -> np.ndarray:
     """log p for slacks sigma = D - t (array), Eq. 2 bin by bin:
          t <  D - l2:        (h/(E[L] b)) (e^{b l2} - e^{b l1}) e^{-b D} e^{b t}
          D - l2 <= t < D - l1: h/(E[L] b) - (h/(E[L] b)) e^{b l1} e^{-b D} e^{b t}
@@ -59,15 +79,15 @@ def log_priority(pm, a, w, b, sigma) -> np.ndarray:
        with c = 1 and h = pm_i / w, combined p = sum_i p_i.  Each term is
        evaluated as its logarithm (e^{b l2} e^{-bD} e^{bt} = e^{-b(sigma - l2)})
        and the sum by logaddexp, so no term overflows."""
-    pm = np.asarray(pm, dtype=np.float64)
+    lpm = np.asarray(lpm, dtype=np.float64)
     sig = np.atleast_1d(np.asarray(sigma, dtype=np.float64))
-    EL = expected_latency(pm, a, w)
+    EL = expected_latency(np.exp(lpm), a, w)
     out = np.full(sig.shape, -np.inf)
-    for i in range(1, len(pm) + 1):
-        if pm[i - 1] <= 0.0:
+    for i in range(1, len(lpm) + 1):
+        if lpm[i - 1] == -np.inf:
             continue
         l1, l2 = a + w * (i - 1), a + w * i
-        logh_b = np.log(pm[i - 1] / w / b)
+        logh_b = lpm[i - 1] - np.log(w * b)  # log(h / b), h = pm_i / w
         term = np.full(sig.shape, -np.inf)
         full = sig >= l2
         part = (sig > l1) & (sig < l2)
@@ -89,8 +109,43 @@ def scores(counts, a, w, num_sizes, b, offsets, deadline, now, weights=None, sto
     for q in range(len(off) - 1):
         sig[off[q]:off[q + 1]] = dl[off[q]:off[q + 1]] - int(now[q])
     for bs in range(1, num_sizes + 1):
-        pm = batch_latency_pmf(counts, bs, weights, store_fp32)
-        out[:, bs - 1] = log_priority(pm, float(a[bs - 1]), float(w[bs - 1]), b, sig)
+        lpm = batch_latency_logpmf(counts, bs, weights, store_fp32)
+        out[:, bs - 1] = log_priority_lp(lpm, float(a[bs - 1]), float(w[bs - 1]), b, sig)
+    return out
+
+
+def log_priority_steps(pm, a, w, b, sigma, offsets, costs) -> np.ndarray:
+    with np.errstate(divide="ignore"):
+        return log_priority_steps_lp(np.log(np.asarray(pm, dtype=np.float64)), a, w, b, sigma, offsets, costs)
+
+
+def log_priority_steps_lp(lpm, a, w, b, sigma, offsets, costs) -> np.ndarray:
+    """Piecewise-step cost (Appendix): deadlines D + offsets[s]
+    with cumulative costs costs[s] decompose into single steps (deadline
+    D + offsets[s], cost costs[s] - costs[s-1]); the priority is the sum of
+    the single-step priorities (each Eq. 2 with c = that increment)."""
+    sig = np.atleast_1d(np.asarray(sigma, dtype=np.float64))
+    out = np.full(sig.shape, -np.inf)
+    prev = 0.0
+    for off, c in zip(offsets, costs):
+        out = np.logaddexp(out, np.log(c - prev) + log_priority_lp(lpm, a, w, b, sig + off))
+        prev = c
+    return out
+
+
+def scores_steps(counts, a, w, num_sizes, b, offsets, deadline, now, step_offsets, step_costs, weights=None,
+                 store_fp32=False) -> np.ndarray:
+    """log p [N][num_sizes] under a piecewise-step cost (see log_priority_steps)."""
+    off = np.asarray(offsets, dtype=np.int64) - int(offsets[0])
+    dl = np.asarray(deadline, dtype=np.int64)
+    out = np.empty((int(off[-1]), num_sizes))
+    sig = np.empty(int(off[-1]), dtype=np.int64)
+    for q in range(len(off) - 1):
+        sig[off[q]:off[q + 1]] = dl[off[q]:off[q + 1]] - int(now[q])
+    for bs in range(1, num_sizes + 1):
+        lpm = batch_latency_logpmf(counts, bs, weights, store_fp32)
+        out[:, bs - 1] = log_priority_steps_lp(lpm, float(a[bs - 1]), float(w[bs - 1]), b, sig, step_offsets,
+                                               step_costs)
     return out
 
 

@@ -254,13 +254,26 @@ class PriorityTable:
                                                    self.log_table.data_ptr(), self.log_expected.data_ptr(),
                                                    _stream_ptr(stream)))
 
-    def scores(self, queues: Queues, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    def scores(self, queues: Queues, out: Optional[torch.Tensor] = None, stream=None, steps=None) -> torch.Tensor:
+        """log p [S][N].  steps = (offset_ticks, cumulative_costs): piecewise-step
+        cost, deadlines D_r + offset with cost c_s after each."""
         N = queues.deadline.numel()
         if out is None:
             out = torch.empty((self.S, N), dtype=torch.float32, device=queues.now.device)
-        _abi.check(_abi.lib().orloj_priority_scores(self.store.c(), self.profile.c(), self.S, self.b,
-                                                    self.log_table.data_ptr(), self.log_expected.data_ptr(),
-                                                    queues.c(), _ptr(out), _stream_ptr(stream)))
+        if steps is None:
+            _abi.check(_abi.lib().orloj_priority_scores(self.store.c(), self.profile.c(), self.S, self.b,
+                                                        self.log_table.data_ptr(), self.log_expected.data_ptr(),
+                                                        queues.c(), _ptr(out), _stream_ptr(stream)))
+        else:
+            off = np.ascontiguousarray(steps[0], dtype=np.int64)
+            cost = np.ascontiguousarray(steps[1], dtype=np.float64)
+            if off.shape != cost.shape or off.ndim != 1:
+                raise OrlojError(1, "steps: offsets and costs must be 1-D of equal length")
+            cs = _abi.CostSteps(len(off), off.ctypes.data, cost.ctypes.data)
+            _abi.check(_abi.lib().orloj_priority_scores_steps(self.store.c(), self.profile.c(), self.S, self.b,
+                                                              self.log_table.data_ptr(), self.log_expected.data_ptr(),
+                                                              queues.c(), ctypes.byref(cs), _ptr(out),
+                                                              _stream_ptr(stream)))
         return out
 
     def pop(self, queues: Queues, log_priority: torch.Tensor, batch_size: torch.Tensor, stream=None,

@@ -61,6 +61,10 @@ class ReplayPolicyC(ctypes.Structure):
     _fields_ = [("objective", ctypes.c_int32), ("drop_threshold_ticks", ctypes.c_void_p)]
 
 
+class CostSteps(ctypes.Structure):
+    _fields_ = [("num_steps", ctypes.c_int32), ("offset_ticks", ctypes.c_void_p), ("cost", ctypes.c_void_p)]
+
+
 class Counters(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("total", "finished", "dropped", "late", "batches", "busy_ticks", "span_ticks")]
@@ -87,6 +91,9 @@ SIGNATURES = {
                                             _P, ctypes.c_double, _P, _P, _P]),
     "orloj_priority_scores": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,
                                              ctypes.c_double, _P, _P, ctypes.POINTER(QueuesC), _P, _P]),
+    "orloj_priority_scores_steps": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                                   ctypes.c_int32, ctypes.c_double, _P, _P, ctypes.POINTER(QueuesC),
+                                                   ctypes.POINTER(CostSteps), _P, _P]),
     "orloj_pop_batch": (ctypes.c_int, [ctypes.POINTER(QueuesC), _P, ctypes.c_int32, _P, _P, _P]),
     "orloj_histogram_accumulate": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int32,
                                                   ctypes.c_int32, _P]),

@@ -165,18 +165,6 @@ cudaError_t launch_score(const ScoreParams &p, bool pick, int64_t store_bytes, c
   return pick ? launch_score_b<true>(p, src, s) : launch_score_b<false>(p, src, s);
 }
 
-template <bool SMEM_TABLE>
-cudaError_t prio_attr() {
-  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
-  if (!configured.load(std::memory_order_acquire)) {
-    const cudaError_t e = cudaFuncSetAttribute(priority_scores_kernel<SMEM_TABLE>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_release);
-  }
-  return cudaSuccess;
-}
-
 orloj_status prepare_score(const orloj_store *store, const orloj_latency_profile *profile,
                            const orloj_queues *queues, ScoreParams *p) {
   orloj_status st;
@@ -216,6 +204,76 @@ orloj_status alloc_flag(unsigned int **dflag, cudaStream_t s) {
   if (cudaMemsetAsync(*dflag, 0, sizeof(unsigned), s) != cudaSuccess)
     return fail(ORLOJ_ERR_CUDA, "memset of validation scratch failed");
   return ORLOJ_OK;
+}
+
+template <bool SMEM_TABLE, bool STEPS>
+cudaError_t prio_launch(unsigned grid, size_t smem, cudaStream_t s, const double *log_table,
+                        const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
+                        const StepsDev &steps, const orloj_queues *q, float *out) {
+  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
+  if (!configured.load(std::memory_order_acquire)) {
+    const cudaError_t e = cudaFuncSetAttribute(priority_scores_kernel<SMEM_TABLE, STEPS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_release);
+  }
+  priority_scores_kernel<SMEM_TABLE, STEPS><<<grid, 256, smem, s>>>(log_table, log_expected, S, B, b, prof, steps,
+                                                                    q->num_queues, q->queue_offsets,
+                                                                    q->deadline_ticks, q->now_ticks, out);
+  return cudaGetLastError();
+}
+
+orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
+                                  double b, const double *log_table, const double *log_expected,
+                                  const orloj_queues *queues, const orloj_cost_steps *cs, float *out,
+                                  void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
+  if ((st = check_queues(queues))) return st;
+  ProfileDev prof;
+  if ((st = compile_profile(profile, store->num_bins, ORLOJ_MAX_KMAX, &prof))) return st;
+  if (S < 1 || S > profile->kmax || !(b > 0.0) || !log_table || !log_expected)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores: need 1 <= num_sizes <= kmax, b > 0, tables");
+  StepsDev steps;
+  std::memset(&steps, 0, sizeof(steps));
+  if (cs) {
+    if (cs->num_steps < 1 || cs->num_steps > PRIO_MAX_STEPS || !cs->offset_ticks || !cs->cost)
+      return fail(ORLOJ_ERR_INVALID_ARGUMENT, "cost steps: need 1..%d steps and both arrays", PRIO_MAX_STEPS);
+    double prev_c = 0.0;
+    for (int i = 0; i < cs->num_steps; ++i) {
+      const int64_t o = cs->offset_ticks[i];
+      const double dc = cs->cost[i] - prev_c;
+      if ((i > 0 && o <= cs->offset_ticks[i - 1]) || o < -(1ll << 40) || o > (1ll << 40) || !(dc > 0.0))
+        return fail(ORLOJ_ERR_INVALID_ARGUMENT,
+                    "cost steps: offsets must increase (|offset| <= 2^40) and costs strictly increase from 0");
+      steps.off[steps.n] = o;
+      steps.logdc[steps.n] = (float)std::log(dc);
+      steps.boff[steps.n] = b * (double)o;
+      ++steps.n;
+      prev_c = cs->cost[i];
+    }
+  }
+  if (queues->num_queues == 0) return ok();
+  if (!out) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores: output is NULL");
+  // Grid-stride over queues: ~resident blocks, so the per-size constants are
+  // staged once per block, not once per 8 queues.
+  const int B = store->num_bins;
+  const bool smem_table = PrioSmem::table_bytes(S, B) <= (64u << 10);
+  const size_t smem = PrioSmem::bytes(S, B, smem_table);
+  const int64_t want = (queues->num_queues + 7) / 8;
+  const int per_sm = smem <= (24u << 10) ? 8 : (int)((200u << 10) / smem);
+  const int64_t cap = (int64_t)148 * (per_sm < 1 ? 1 : per_sm);
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (cs)
+    e = smem_table ? prio_launch<true, true>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out)
+                   : prio_launch<false, true>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out);
+  else
+    e = smem_table ? prio_launch<true, false>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out)
+                   : prio_launch<false, false>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out);
+  if (e != cudaSuccess) return cuda_fail(e, "priority_scores launch");
+  return ok();
 }
 
 }  // namespace
@@ -404,40 +462,19 @@ orloj_status orloj_priority_table(const orloj_store *store, const orloj_latency_
   return ok();
 }
 
+
 orloj_status orloj_priority_scores(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
                                    double b, const double *log_table, const double *log_expected,
                                    const orloj_queues *queues, float *out, void *stream) {
-  orloj_status st;
-  if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
-  if ((st = check_queues(queues))) return st;
-  ProfileDev prof;
-  if ((st = compile_profile(profile, store->num_bins, ORLOJ_MAX_KMAX, &prof))) return st;
-  if (S < 1 || S > profile->kmax || !(b > 0.0) || !log_table || !log_expected)
-    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores: need 1 <= num_sizes <= kmax, b > 0, tables");
-  if (queues->num_queues == 0) return ok();
-  if (!out) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores: output is NULL");
-  // Grid-stride over queues: ~resident blocks, so the per-size constants are
-  // staged once per block, not once per 8 queues.
-  const int B = store->num_bins;
-  const bool smem_table = PrioSmem::table_bytes(S, B) <= (64u << 10);
-  const size_t smem = PrioSmem::bytes(S, B, smem_table);
-  cudaError_t e = smem_table ? prio_attr<true>() : prio_attr<false>();
-  if (e != cudaSuccess) return cuda_fail(e, "priority_scores attributes");
-  const int64_t want = (queues->num_queues + 7) / 8;
-  const int per_sm = smem <= (24u << 10) ? 8 : (int)((200u << 10) / smem);
-  const int64_t cap = (int64_t)148 * (per_sm < 1 ? 1 : per_sm);
-  const unsigned grid = (unsigned)(want < cap ? want : cap);
-  if (smem_table)
-    priority_scores_kernel<true><<<grid, 256, smem, (cudaStream_t)stream>>>(
-        log_table, log_expected, S, B, b, prof, queues->num_queues, queues->queue_offsets, queues->deadline_ticks,
-        queues->now_ticks, out);
-  else
-    priority_scores_kernel<false><<<grid, 256, smem, (cudaStream_t)stream>>>(
-        log_table, log_expected, S, B, b, prof, queues->num_queues, queues->queue_offsets, queues->deadline_ticks,
-        queues->now_ticks, out);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "priority_scores launch");
-  return ok();
+  return priority_scores_impl(store, profile, S, b, log_table, log_expected, queues, nullptr, out, stream);
+}
+
+orloj_status orloj_priority_scores_steps(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
+                                         double b, const double *log_table, const double *log_expected,
+                                         const orloj_queues *queues, const orloj_cost_steps *steps, float *out,
+                                         void *stream) {
+  if (!steps) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores_steps: steps is NULL");
+  return priority_scores_impl(store, profile, S, b, log_table, log_expected, queues, steps, out, stream);
 }
 
 orloj_status orloj_pop_batch(const orloj_queues *queues, const float *logp, int32_t S, const int32_t *bs,

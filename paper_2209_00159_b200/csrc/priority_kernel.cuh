@@ -44,15 +44,18 @@ __global__ void priority_table_kernel(const float *__restrict__ log2F, int32_t D
   C[0] = -INFINITY;
   H[0] = -INFINITY;
   const double lgw = log(expm1(b * w));  // log(e^{bw} - 1)
-  double prevG = 0.0, acc = -INFINITY, mean_bin = 0.0;
+  const double lwb = log(w * b);
+  // log G_i = bs log F_mix(tau_i) and log pm_i = log G_i + log(1 - G_{i-1}/G_i):
+  // no underflow (F^bs leaves the fp64 range for small F and large bs)
+  double prevlG = -INFINITY, acc = -INFINITY, mean_bin = 0.0;
   for (int i = 1; i <= B; ++i) {
-    const double G = pow(s_mix[i - 1], (double)bs);
-    const double pm = G - prevG;
-    prevG = G;
-    mean_bin += pm * (i - 0.5);
+    const double lG = s_mix[i - 1] > 0.0 ? (double)bs * log(s_mix[i - 1]) : -INFINITY;
+    const double lpm = lG > prevlG ? lG + log(-expm1(prevlG - lG)) : -INFINITY;
+    prevlG = lG;
+    mean_bin += exp(lpm) * (i - 0.5);
     double h = -INFINITY;
-    if (pm > 0.0) {
-      h = log(pm / (w * b));
+    if (lpm > -INFINITY) {
+      h = lpm - lwb;
       const double x = h + b * (a + w * (i - 1)) + lgw;
       const double m = acc > x ? acc : x;
       acc = m + log(exp(acc - m) + exp(x - m));
@@ -85,12 +88,28 @@ struct PrioSmem {
 };
 
 constexpr int PRIO_CHUNK = 8;  // members per lane per pass
+constexpr int PRIO_MAX_STEPS = 8;
 
-template <bool SMEM_TABLE>
+// Piecewise-step cost: deadlines D_r + off[s] with cost
+// increments dc[s] = c_s - c_{s-1} > 0; p = sum_s dc[s] p_single(sigma + off[s]).
+struct StepsDev {
+  int32_t n;
+  int64_t off[PRIO_MAX_STEPS];
+  float logdc[PRIO_MAX_STEPS];   // log dc[s]
+  double boff[PRIO_MAX_STEPS];   // b off[s]
+};
+
+__device__ __forceinline__ float logaddexpf_(float a, float b) {
+  const float M = fmaxf(a, b);
+  return M == -INFINITY ? M : M + log1pf(__expf(fminf(a, b) - M));
+}
+
+template <bool SMEM_TABLE, bool STEPS>
 __global__ void __launch_bounds__(256) priority_scores_kernel(
     const double *__restrict__ table, const double *__restrict__ logEL, int32_t S, int32_t B, double b,
-    const __grid_constant__ ProfileDev prof, int64_t Q, const int64_t *__restrict__ offsets,
-    const int64_t *__restrict__ deadline, const int64_t *__restrict__ now, float *__restrict__ out) {
+    const __grid_constant__ ProfileDev prof, const __grid_constant__ StepsDev steps, int64_t Q,
+    const int64_t *__restrict__ offsets, const int64_t *__restrict__ deadline, const int64_t *__restrict__ now,
+    float *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int4 *s_lk = reinterpret_cast<int4 *>(smem_raw);                                          // [S]
   double *s_C = reinterpret_cast<double *>(s_lk + S);                                       // [S][B+1]
@@ -112,16 +131,44 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
   const float bf = (float)b;
   const int64_t base0 = offsets[0], N = offsets[Q] - base0;
   const int64_t wpb = blockDim.x >> 5;
+
+  // log p_single for size k at slack sigma (s2 = sigma2(sigma), bsig = -b sigma)
+  auto single = [&](int k, const int4 &lk, int32_t w, double lEL, int32_t s2, double bsig) -> float {
+    const int i = lookup_bin(s2, lk.x, lk.y, (uint32_t)lk.z, (uint32_t)lk.w);
+    // x = sigma - l1 of bin i+1 (exact: below the horizon 2 sigma - 2a fits int32;
+    // sigma < 0 gives x = -a <= 0)
+    const int32_t x = ((s2 - lk.x) >> 1) - w * i;
+    const bool part = i < B && x > 0;
+    double Ci;
+    float Hn = -INFINITY;
+    if (SMEM_TABLE) {
+      Ci = s_C[k * (B + 1) + i];
+      if (part) Hn = s_H[k * (B + 1) + i + 1];
+    } else {
+      Ci = table[(size_t)k * 2 * (B + 1) + i] - lEL;
+      if (part) Hn = (float)(table[(size_t)k * 2 * (B + 1) + B + 1 + i + 1] - lEL);
+    }
+    float lp = (float)(Ci + bsig);
+    if (Hn > -INFINITY) {
+      const float g = -expm1f(-bf * (float)x);  // 1 - e^{-b x}, 0 < b x < b w
+      const float M = fmaxf(lp, Hn);
+      lp = M + logf(__expf(lp - M) + __expf(Hn - M) * g);
+    }
+    return lp;
+  };
+
   for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < Q; q += (int64_t)gridDim.x * wpb) {
     const int64_t b0 = offsets[q] - base0, e0 = offsets[q + 1] - base0;
     const int64_t t = now[q];
     for (int64_t c0 = b0; c0 < e0; c0 += 32 * PRIO_CHUNK) {
       double bsig[PRIO_CHUNK];  // -b sigma
+      int64_t sg[PRIO_CHUNK];   // sigma (STEPS)
       int32_t s2[PRIO_CHUNK];
 #pragma unroll
       for (int m = 0; m < PRIO_CHUNK; ++m) {
         const int64_t j = c0 + lane + 32 * m;
         const int64_t sigma = j < e0 ? deadline[j] - t : 0;
+        sg[m] = sigma;
         bsig[m] = -b * (double)sigma;
         s2[m] = sigma2(sigma);
       }
@@ -134,25 +181,14 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
         for (int m = 0; m < PRIO_CHUNK; ++m) {
           const int64_t j = c0 + lane + 32 * m;
           if (j >= e0) break;
-          const int i = lookup_bin(s2[m], lk.x, lk.y, (uint32_t)lk.z, (uint32_t)lk.w);
-          // x = sigma - l1 of bin i+1 (exact: below the horizon 2 sigma - 2a fits int32;
-          // sigma < 0 gives x = -a <= 0)
-          const int32_t x = ((s2[m] - lk.x) >> 1) - w * i;
-          const bool part = i < B && x > 0;
-          double Ci;
-          float Hn = -INFINITY;
-          if (SMEM_TABLE) {
-            Ci = s_C[k * (B + 1) + i];
-            if (part) Hn = s_H[k * (B + 1) + i + 1];
+          float lp;
+          if (STEPS) {
+            lp = -INFINITY;
+            for (int st = 0; st < steps.n; ++st)
+              lp = logaddexpf_(lp, steps.logdc[st] + single(k, lk, w, lEL, sigma2(sg[m] + steps.off[st]),
+                                                           bsig[m] - steps.boff[st]));
           } else {
-            Ci = table[(size_t)k * 2 * (B + 1) + i] - lEL;
-            if (part) Hn = (float)(table[(size_t)k * 2 * (B + 1) + B + 1 + i + 1] - lEL);
-          }
-          float lp = (float)(Ci + bsig[m]);
-          if (Hn > -INFINITY) {
-            const float g = -expm1f(-bf * (float)x);  // 1 - e^{-b x}, 0 < b x < b w
-            const float M = fmaxf(lp, Hn);
-            lp = M + logf(__expf(lp - M) + __expf(Hn - M) * g);
+            lp = single(k, lk, w, lEL, s2[m], bsig[m]);
           }
           ok[j] = lp;
         }

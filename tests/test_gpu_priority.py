@@ -178,3 +178,30 @@ def test_scores_then_pop_selects_the_top():
         if want:
             kth = rows[want[-1]]
             assert all(rows[r] >= kth - 2 * _tol(kth) for r in got)
+
+
+@pytest.mark.parametrize("name", ["skipnet", "gpt"])
+def test_piecewise_step_scores_vs_oracle(name):
+    """orloj_priority_scores_steps vs the oracle's sum of
+    single-step priorities; each step is the single-step arithmetic (same
+    tolerance per term) combined by an fp32 log-add-exp."""
+    fam, prof, q = _case(name, gen.SEED_BASE + 920, Q=64)
+    b = 1.0 / fam.mean_ticks()
+    p99 = fam.p99_ticks()
+    offs, costs = [-p99 // 4, 0, p99 // 2], [0.25, 1.0, 1.75]
+    tab, qs, _ = _gpu_scores(fam, prof, q, b)
+    lp = tab.scores(qs, steps=(offs, costs))
+    single = tab.scores(qs, steps=([0], [1.0]))
+    base = tab.scores(qs)
+    torch.cuda.synchronize()
+    assert torch.equal(single, base)  # one unit step is the plain priority, bit for bit
+    got = lp.cpu().numpy().T.astype(np.float64)
+    ref = pr.scores_steps(fam.counts, prof.a, prof.w, S, b, q.offsets, q.deadline, q.now, offs, costs,
+                          store_fp32=True)
+    ninf = ref == -np.inf
+    assert (np.isneginf(got) == ninf).all()
+    err = np.abs(got[~ninf] - ref[~ninf])
+    assert (err <= 3e-6 + 2.0 ** -21 * np.abs(ref[~ninf])).all(), float(err.max())
+    for bad in (([0, 0], [1.0, 2.0]), ([0, 5], [1.0, 1.0]), ([0], [0.0]), (list(range(9)), [float(i + 1) for i in range(9)])):
+        with pytest.raises(orj.OrlojError):
+            tab.scores(qs, steps=bad)

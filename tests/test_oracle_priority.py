@@ -10,7 +10,9 @@ oracle's own formulas:
 * E[L] against the quadrature of the survival function;
 * the limits b -> 0 (p -> P(L <= sigma) / E[L]) and the milestone form
   p(t) = alpha e^{bt} + beta between milestones (P:602-607);
-* PopBatch against the order invariants of "the bs highest priorities".
+* PopBatch against the order invariants of "the bs highest priorities";
+* the piecewise-step cost against Eq. 1 with the multi-step
+  cost function itself, by quadrature.
 """
 import itertools
 import math
@@ -152,3 +154,63 @@ def test_pop_batch_invariants():
                 assert (col[sel[j - 1]], -sel[j - 1]) > (col[r], -r)
             for u in rest:  # every unselected candidate is lower, or equal and later
                 assert (col[r], -r) > (col[u], -u)
+
+
+def test_piecewise_step_cost_matches_definition():
+    """Appendix: with a multi-step cost C(x) = c_s for finish
+    times x in (D + off_s, D + off_{s+1}] (c_0 = 0 before the first deadline),
+    Eq. 1's E[C_delay] - E[C_now] evaluated from that definition by quadrature
+    equals the oracle's sum of single-step priorities."""
+    counts = _fam()
+    a, w, b, bs = 250.0, 100.0, 3e-3, 2
+    offs, costs = [0.0, 150.0, 420.0], [1.0, 2.5, 3.0]
+    pm = pr.batch_latency_pmf(counts, bs)
+    F, edges = _F_L(pm, a, w)
+    EL = pr.expected_latency(pm, a, w)
+
+    def cdf_conv(y):  # P(tau + L <= y)
+        if y <= 0:
+            return 0.0
+        pts = [y - e for e in edges if 0 < y - e < y]
+        return integrate.quad(lambda u: b * math.exp(-b * u) * F(y - u), 0.0, y, points=pts or None, limit=400,
+                              epsabs=1e-15, epsrel=1e-12)[0]
+
+    def expected_cost(cdf, sigma):  # E[C] with finish time measured from now: x <= sigma + off_s is on time for s
+        lv = [cdf(sigma + o) for o in offs]  # P(finish within deadline s)
+        # cost c_{s} applies when finishing after deadline s but within deadline s+1 (c_last after the last)
+        e = 0.0
+        for s in range(len(offs)):
+            p_after_s = 1.0 - lv[s]
+            p_after_next = 1.0 - lv[s + 1] if s + 1 < len(offs) else 0.0
+            e += costs[s] * (p_after_s - p_after_next)
+        return e
+
+    for s in (a + 0.5 * w, a + 2.3 * w, a + 5 * w, edges[-1] + 100, edges[-1] + 600):
+        p_def = (expected_cost(cdf_conv, s) - expected_cost(F, s)) / EL
+        got = math.exp(pr.log_priority_steps(pm, a, w, b, [s], offs, costs)[0])
+        assert abs(got - p_def) <= 1e-9 * p_def + 1e-15, (s, got, p_def)
+    # one step with cost 1 at offset 0 is the single-step priority
+    sig = np.array([a + 1.5 * w, a + 4 * w])
+    assert np.array_equal(pr.log_priority_steps(pm, a, w, b, sig, [0.0], [1.0]), pr.log_priority(pm, a, w, b, sig))
+
+
+@pytest.mark.parametrize("bs", [1, 8, 40])
+def test_batch_logpmf_exact_rationals_beyond_fp64_range(bs):
+    """log pm_i against exact rational arithmetic, including bin masses far
+    below the fp64 range (F = 2^-20 in the first bin, bs = 40: G = 2^-800)."""
+    from fractions import Fraction
+    counts = np.array([[1, 0, 5, 1000, 2**20 - 1006], [0, 3, 0, 7, 2**20 - 10]], dtype=np.int64)
+    T = 2**20
+    Fmix = [(Fraction(int(counts[0, :i + 1].sum()), T) + Fraction(int(counts[1, :i + 1].sum()), T)) / 2
+            for i in range(counts.shape[1])]
+    G = [f ** bs for f in Fmix]
+    got = pr.batch_latency_logpmf(counts, bs)
+    prev = Fraction(0)
+    for i, g in enumerate(G):
+        pm = g - prev
+        prev = g
+        if pm == 0:
+            assert got[i] == -np.inf
+        else:
+            want = math.log(pm.numerator) - math.log(pm.denominator)
+            assert abs(got[i] - want) <= 1e-12 * max(1.0, abs(want)), (i, got[i], want)
