@@ -547,6 +547,29 @@ def run_policies(args, rank, world, dev):
                 "finish_rate_by_bucket": {f.tf.fam.name: [round(float(x), 4) for x in c[i, :, 1] / np.maximum(c[i, :, 0], 1)]
                                           for i, f in enumerate(fams)},
                 "dropped_frac": round(float(c[:, :, 2].sum() / max(c[:, :, 0].sum(), 1)), 4)}
+    # the paper's scheduler iteration (Alg. 1): per-size feasibility by E[L_bs] of the
+    # all-application batch model, earliest-deadline candidate size, PopBatch by Eq. 1-2 priority
+    tabs = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
+    setup = []
+    for f in fams:
+        pt = orj.PriorityTable(f.store, f.profile, f.profile.kmax, 1.0 / f.tf.fam.mean_ticks())
+        st = torch.from_numpy(policy.alg1_size_thresholds(f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).to(dev)
+        setup.append((pt, st))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for f, t_, (pt, st) in zip(fams, tabs, setup):
+        orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, objective="alg1", priority=pt,
+                         size_thresholds=st)
+    e1.record()
+    parallel.allreduce_counters(tabs)
+    torch.cuda.synchronize()
+    c = tabs.cpu().numpy()
+    out["alg1 (Eq. 1-2 PopBatch, b = 1/mean)"] = {
+        "ms": e0.elapsed_time(e1),
+        "finish_rate_by_bucket": {f.tf.fam.name: [round(float(x), 4) for x in c[i, :, 1] / np.maximum(c[i, :, 0], 1)]
+                                  for i, f in enumerate(fams)},
+        "dropped_frac": round(float(c[:, :, 2].sum() / max(c[:, :, 0].sum(), 1)), 4)}
     return out
 
 

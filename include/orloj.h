@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define ORLOJ_ABI_VERSION 1
+#define ORLOJ_ABI_VERSION 2
 #define ORLOJ_MAX_KMAX 256        /* candidate batch sizes per queue (score / pick) */
 #define ORLOJ_MAX_BINS 256        /* bins per histogram (score / pick) */
 #define ORLOJ_REPLAY_MAX_KMAX 32  /* window size in replay */
@@ -227,10 +227,27 @@ orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_pr
  * thr[d] = a_1 + ceil(w_1 E[bin_d]) (an integer the caller computes from the
  * histogram counts).  Thresholds are assumed non-negative and fixed per replay
  * (dropping stays permanent only if thr[d] <= a_1 + w_1 B). */
-typedef enum { ORLOJ_OBJ_EXPECTED_FINISH = 0, ORLOJ_OBJ_FINISH_RATE = 1 } orloj_objective;
+/* ORLOJ_OBJ_ALG1 replays the paper's scheduler iteration (Alg. 1)
+ * over the window (the kmax earliest-deadline pending requests, A9):
+ *   drop (l.10-13): r leaves every Q_bs iff t + E[L_bs] > D_r for all bs, i.e.
+ *     D_r - t < thr_1 (E[L_bs] is non-decreasing in bs);
+ *   Q_bs = {r : D_r - t >= thr_bs}, thr_bs = ceil(E[L_bs]) of the
+ *     all-application batch model (integer ticks, so the test is exact);
+ *   candidate (l.14-19): among bs with |Q_bs| >= bs the earliest D_{Q_bs}, ties ->
+ *     larger bs (the prose "overall earliest deadline" reading of l.15);
+ *   PopBatch (l.20): the bs members of Q_bs with the highest Eq. 1-2 priority
+ *     (orloj_priority_table tables, ties -> earlier member); the rest stay pending.
+ * The decision log then holds, per decision, the bit mask of popped window
+ * positions (bit r = r-th earliest-deadline pending member). */
+typedef enum { ORLOJ_OBJ_EXPECTED_FINISH = 0, ORLOJ_OBJ_FINISH_RATE = 1, ORLOJ_OBJ_ALG1 = 2 } orloj_objective;
 typedef struct {
   int32_t objective;                   /* orloj_objective */
-  const int64_t *drop_threshold_ticks; /* device [num_dists] or NULL (hopeless rule) */
+  const int64_t *drop_threshold_ticks; /* device [num_dists] or NULL (hopeless rule); NULL for ALG1 */
+  /* ALG1 only (NULL / 0 otherwise): */
+  const int64_t *size_threshold_ticks;  /* device [kmax]: thr_bs = ceil(E[L_bs]), non-decreasing, >= 0 */
+  const double *priority_table;         /* device [kmax][2][B+1] (orloj_priority_table, num_sizes = kmax) */
+  const double *priority_log_expected;  /* device [kmax] */
+  double priority_b_per_tick;           /* the b the tables were built with */
 } orloj_replay_policy;
 orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency_profile *profile,
                                    const orloj_trace *trace, const orloj_replay_policy *policy,

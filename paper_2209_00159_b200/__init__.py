@@ -392,17 +392,22 @@ class Trace:
         return ctypes.byref(self._c)
 
 
-OBJECTIVES = {"expected_finish": 0, "finish_rate": 1}
+OBJECTIVES = {"expected_finish": 0, "finish_rate": 1, "alg1": 2}
 
 
 def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, per_bucket=None,
                  decision_log: bool | torch.Tensor = False, stream=None, objective: str = "expected_finish",
-                 drop_threshold: Optional[torch.Tensor] = None):
+                 drop_threshold: Optional[torch.Tensor] = None, priority: Optional["PriorityTable"] = None,
+                 size_thresholds: Optional[torch.Tensor] = None):
     """Replay every scenario; returns (per_bucket int64 [num_buckets, 7], log or None).
     per_bucket is ADDED to (pass a zeroed tensor to accumulate across calls).
     objective: "expected_finish" (argmax E_k) or "finish_rate" (argmax
     E_k / E[L_{B_k}]); drop_threshold: device int64 [num_dists] (see
-    policy.expected_latency_thresholds) or None for the hopeless rule."""
+    policy.expected_latency_thresholds) or None for the hopeless rule.
+    objective "alg1" (the paper's Alg. 1 iteration, include/orloj.h) needs
+    `priority` (a PriorityTable with num_sizes = kmax) and `size_thresholds`
+    (device int64 [kmax], policy.alg1_size_thresholds); the decision log then
+    holds popped-member bit masks."""
     dev = trace.arrival.device
     if per_bucket is None:
         per_bucket = torch.zeros((trace.num_buckets, 7), dtype=torch.int64, device=dev)
@@ -418,7 +423,19 @@ def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, p
         _dev(drop_threshold, torch.int64, "drop_threshold")
         if drop_threshold.numel() != store.num_dists:
             raise OrlojError(1, "drop_threshold must have one entry per distribution")
-    pol = _abi.ReplayPolicyC(OBJECTIVES[objective], _ptr(drop_threshold))
+    pol = _abi.ReplayPolicyC(OBJECTIVES[objective], _ptr(drop_threshold), None, None, None, 0.0)
+    if objective == "alg1":
+        if priority is None or size_thresholds is None:
+            raise OrlojError(1, "objective alg1 needs priority tables and size thresholds")
+        if priority.S != profile.kmax:
+            raise OrlojError(1, "alg1: the priority tables must cover batch sizes 1..kmax")
+        _dev(size_thresholds, torch.int64, "size_thresholds")
+        if size_thresholds.numel() != profile.kmax:
+            raise OrlojError(1, "size_thresholds must have kmax entries")
+        pol.size_threshold_ticks = size_thresholds.data_ptr()
+        pol.priority_table = priority.log_table.data_ptr()
+        pol.priority_log_expected = priority.log_expected.data_ptr()
+        pol.priority_b_per_tick = priority.b
     _abi.check(_abi.lib().orloj_replay_trace_ex(store.c(), profile.c(), trace.c(), ctypes.byref(pol),
                                                 per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
     return per_bucket, log

@@ -58,7 +58,9 @@ class TraceC(ctypes.Structure):
 
 
 class ReplayPolicyC(ctypes.Structure):
-    _fields_ = [("objective", ctypes.c_int32), ("drop_threshold_ticks", ctypes.c_void_p)]
+    _fields_ = [("objective", ctypes.c_int32), ("drop_threshold_ticks", ctypes.c_void_p),
+                ("size_threshold_ticks", ctypes.c_void_p), ("priority_table", ctypes.c_void_p),
+                ("priority_log_expected", ctypes.c_void_p), ("priority_b_per_tick", ctypes.c_double)]
 
 
 class CostSteps(ctypes.Structure):

@@ -373,7 +373,7 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
 
 orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
                                 const orloj_trace *tr, orloj_counters *per_bucket, int32_t *log, void *stream) {
-  const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr};
+  const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
   return orloj_replay_trace_ex(store, profile, tr, &def, per_bucket, log, stream);
 }
 
@@ -382,9 +382,16 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
                                    orloj_counters *per_bucket, int32_t *log, void *stream) {
   orloj_status st;
   if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
-  if (!policy || (policy->objective != ORLOJ_OBJ_EXPECTED_FINISH && policy->objective != ORLOJ_OBJ_FINISH_RATE))
-    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay policy: objective must be EXPECTED_FINISH or FINISH_RATE");
+  if (!policy || (policy->objective != ORLOJ_OBJ_EXPECTED_FINISH && policy->objective != ORLOJ_OBJ_FINISH_RATE &&
+                  policy->objective != ORLOJ_OBJ_ALG1))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay policy: objective must be EXPECTED_FINISH, FINISH_RATE or ALG1");
   const bool rate = policy->objective == ORLOJ_OBJ_FINISH_RATE;
+  const bool alg1 = policy->objective == ORLOJ_OBJ_ALG1;
+  if (alg1 && (!policy->size_threshold_ticks || !policy->priority_table || !policy->priority_log_expected ||
+               !(policy->priority_b_per_tick > 0.0) || policy->drop_threshold_ticks))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT,
+                "replay policy ALG1: needs size thresholds, priority tables for sizes 1..kmax and b > 0, "
+                "and no drop thresholds (Alg. 1 drops by the bs = 1 threshold)");
   if (!tr || tr->num_scenarios < 0 || tr->num_buckets < 1)
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace: need num_scenarios >= 0 and num_buckets >= 1");
   if (tr->num_scenarios > 0 && (!tr->arrival_offsets || !tr->arrival_ticks || !tr->dist_id || !tr->true_bin ||
@@ -416,22 +423,32 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
   p.counters = reinterpret_cast<unsigned long long *>(per_bucket);
   p.log = log;
   p.drop_thr = policy->drop_threshold_ticks;
+  if (alg1) {
+    p.size_thr = policy->size_threshold_ticks;
+    p.prio_table = policy->priority_table;
+    p.prio_logEL = policy->priority_log_expected;
+    p.prio_b = policy->priority_b_per_tick;
+  }
   if (p.S == 0) return ok();
   const unsigned blocks = (unsigned)((p.S + REPLAY_WARPS - 1) / REPLAY_WARPS);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  switch (bpl * 2 + (rate ? 1 : 0)) {
-#define ORLOJ_REPLAY_CASE(BPL_, RATE_)                                                                         \
-  case BPL_ * 2 + (RATE_ ? 1 : 0):                                                                             \
-    e = cudaFuncSetAttribute(replay_kernel<BPL_, RATE_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e == cudaSuccess) replay_kernel<BPL_, RATE_><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);               \
+  switch (bpl * 4 + (rate ? 1 : 0) + (alg1 ? 2 : 0)) {
+#define ORLOJ_REPLAY_CASE(BPL_, RATE_, ALG1_)                                                                  \
+  case BPL_ * 4 + (RATE_ ? 1 : 0) + (ALG1_ ? 2 : 0):                                                           \
+    e = cudaFuncSetAttribute(replay_kernel<BPL_, RATE_, ALG1_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                             (int)smem);                                                                       \
+    if (e == cudaSuccess) replay_kernel<BPL_, RATE_, ALG1_><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);        \
     break;
-    ORLOJ_REPLAY_CASE(1, false)
-    ORLOJ_REPLAY_CASE(1, true)
-    ORLOJ_REPLAY_CASE(2, false)
-    ORLOJ_REPLAY_CASE(2, true)
-    ORLOJ_REPLAY_CASE(4, false)
-    ORLOJ_REPLAY_CASE(4, true)
+    ORLOJ_REPLAY_CASE(1, false, false)
+    ORLOJ_REPLAY_CASE(1, true, false)
+    ORLOJ_REPLAY_CASE(1, false, true)
+    ORLOJ_REPLAY_CASE(2, false, false)
+    ORLOJ_REPLAY_CASE(2, true, false)
+    ORLOJ_REPLAY_CASE(2, false, true)
+    ORLOJ_REPLAY_CASE(4, false, false)
+    ORLOJ_REPLAY_CASE(4, true, false)
+    ORLOJ_REPLAY_CASE(4, false, true)
 #undef ORLOJ_REPLAY_CASE
     default:
       return fail(ORLOJ_ERR_CAPACITY, "replay: unsupported bins per lane");

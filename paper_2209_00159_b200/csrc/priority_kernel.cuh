@@ -21,6 +21,13 @@
 
 namespace orloj {
 
+// Order-preserving key of a float (larger float -> larger unsigned key).
+__device__ __forceinline__ uint32_t fkey(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+
 // One block per batch size: mixture CDF, pmf of the max of bs draws, E[L],
 // the full-bin prefix C[0..B] and the per-bin log(h_i / b) H[0..B] (H[0] =
 // -inf), all fp64.  table layout [S][2][B+1]: [s][0][i] = C[i], [s][1][i] = H[i].
@@ -86,6 +93,24 @@ struct PrioSmem {
     return (size_t)S * (16 + 4) + (smem_table ? table_bytes(S, B) : 0);
   }
 };
+
+// One element of the score kernel with the table read from global memory
+// (tab_k = table + (k-1) 2 (B+1)); the same arithmetic, value for value, as the
+// shared-memory path (which stages tab - lEL in fp64 and (float)(tab - lEL)).
+__device__ __forceinline__ float prio_elem_global(const double *__restrict__ tab_k, double lEL, int B, int4 lk,
+                                                  int32_t w, int32_t s2, double bsig, float bf) {
+  const int i = lookup_bin(s2, lk.x, lk.y, (uint32_t)lk.z, (uint32_t)lk.w);
+  const int32_t x = ((s2 - lk.x) >> 1) - w * i;
+  const double Ci = tab_k[i] - lEL;
+  const float Hn = (i < B && x > 0) ? (float)(tab_k[B + 1 + i + 1] - lEL) : -INFINITY;
+  float lp = (float)(Ci + bsig);
+  if (Hn > -INFINITY) {
+    const float g = -expm1f(-bf * (float)x);
+    const float M = fmaxf(lp, Hn);
+    lp = M + logf(__expf(lp - M) + __expf(Hn - M) * g);
+  }
+  return lp;
+}
 
 constexpr int PRIO_CHUNK = 8;  // members per lane per pass
 constexpr int PRIO_MAX_STEPS = 8;
@@ -195,12 +220,6 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
       }
     }
   }
-}
-
-// Order-preserving key of a float (larger float -> larger unsigned key).
-__device__ __forceinline__ uint32_t fkey(float x) {
-  const uint32_t u = __float_as_uint(x);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
 // Compare-exchange for a descending sort of (key, -index) pairs: after it,

@@ -24,6 +24,7 @@
 // Counters are kept warp-uniform and added to per-bucket int64 totals at the end.
 #pragma once
 #include "common.cuh"
+#include "priority_kernel.cuh"
 
 namespace orloj {
 
@@ -41,6 +42,12 @@ struct ReplayParams {
   unsigned long long *counters;  // [num_buckets][7]
   int32_t *log;                  // [N + S] or null
   const int64_t *drop_thr;       // [D] or null: drop iff D_r - t < thr[d_r] (null: hopeless rule)
+  // Alg. 1 policy (ALG1): thr_bs = ceil(E[L_bs]) of the all-application batch
+  // model [kmax]; Eq. 1-2 priority tables [kmax][2][B+1], log E[L] [kmax], b
+  const int64_t *size_thr;
+  const double *prio_table;
+  const double *prio_logEL;
+  double prio_b;
   ProfileDev prof;
 };
 
@@ -72,7 +79,7 @@ __host__ __device__ inline size_t replay_head_bytes(int D, int B) {
 #define ORLOJ_REPLAY_MIN_BLOCKS 8
 #endif
 
-template <int BPL, bool RATE>
+template <int BPL, bool RATE, bool ALG1 = false>
 __global__ void __launch_bounds__(REPLAY_WARPS * 32, ORLOJ_REPLAY_MIN_BLOCKS)
 replay_kernel(const __grid_constant__ ReplayParams p) {
   constexpr int STG = ReplayWarpSmem<BPL, RATE>::STG;
@@ -101,7 +108,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     int m = B;
     for (int i = B - 1; i >= 0; --i)
       if (s_store[d * B + i] != -INFINITY) m = i + 1;
-    s_thr[d] = p.drop_thr ? p.drop_thr[d] : (int64_t)p.prof.a[0] + (int64_t)p.prof.w[0] * m;
+    s_thr[d] = ALG1 ? p.size_thr[0]  // Alg. 1 l.10-13: infeasible for every bs iff infeasible for bs = 1
+                    : p.drop_thr ? p.drop_thr[d] : (int64_t)p.prof.a[0] + (int64_t)p.prof.w[0] * m;
   }
   if (lane < REPLAY_KB) stg[lane * STG - 1] = -INFINITY;
   __syncthreads();
@@ -119,6 +127,13 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   // RATE: lane k-1 evaluates E[L_{B_k}] with a_k, w_k of its own candidate size
   const float my_a = RATE ? (float)p.prof.a[lane] : 0.f;
   const float my_w = RATE ? (float)p.prof.w[lane] : 0.f;
+  // ALG1: lane bs-1 holds thr_bs and the lookup constants of size bs
+  const int64_t my_thr = (ALG1 && lane < kmax) ? p.size_thr[lane] : INT64_MAX;
+  const int4 my_lk = (ALG1 && lane < kmax) ? make_int4(p.prof.a2[lane], p.prof.wB2[lane], (int)p.prof.mag[lane],
+                                                       (int)p.prof.sh[lane])
+                                           : make_int4(0, 0, 0, 0);
+  const int32_t my_wk = (ALG1 && lane < kmax) ? p.prof.w[lane] : 0;
+  const int32_t my_ak = (ALG1 && lane < kmax) ? p.prof.a[lane] : 0;
 
   int64_t t = INT64_MIN;
   int64_t cursor = 0;
@@ -288,7 +303,44 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     const int tb = mem ? w_tb[lane] : 0;
 
     int kstar = 1;  // a window of one has a single candidate: no scoring needed
-    if (wc > 1) {   // warp-uniform
+    uint32_t selm = 1u;  // ALG1: the popped members (window positions)
+    if (ALG1 && wc > 1) {  // warp-uniform
+      // Alg. 1 l.14-20: Q_bs = {r : t + E[L_bs] <= D_r} is a suffix of
+      // the deadline-ordered window; lane bs-1 finds its first member by binary search
+      int lo = 0, hi = wc;
+      const int64_t need = my_thr == INT64_MAX ? INT64_MAX : t + my_thr;  // beyond kmax: never feasible
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (w_dl[mid] < need || my_thr == INT64_MAX) lo = mid + 1;
+        else hi = mid;
+      }
+      const bool feas = lane < kmax && wc - lo >= lane + 1;  // |Q_bs| >= bs
+      // candidate: earliest D_{Q_bs}, ties -> larger bs (SURVEY A/Design reading of P:296-297)
+      const uint64_t dq = feas ? (uint64_t)(w_dl[lo] - t) : ~0ull;  // >= 0 when feasible
+      const uint32_t mh = __reduce_min_sync(FULL, (uint32_t)(dq >> 32));
+      const uint32_t ml = __reduce_min_sync(FULL, (uint32_t)(dq >> 32) == mh ? (uint32_t)dq : 0xffffffffu);
+      kstar = (int)__reduce_max_sync(FULL, (feas && dq == (((uint64_t)mh << 32) | ml)) ? (uint32_t)(lane + 1) : 0u);
+      const int first = __shfl_sync(FULL, lo, kstar - 1);
+      // PopBatch(Q_kstar): the kstar highest Eq. 1-2 priorities, ties -> earlier member
+      const int4 lk = make_int4(__shfl_sync(FULL, my_lk.x, kstar - 1), __shfl_sync(FULL, my_lk.y, kstar - 1),
+                                __shfl_sync(FULL, my_lk.z, kstar - 1), __shfl_sync(FULL, my_lk.w, kstar - 1));
+      const int32_t wk = __shfl_sync(FULL, my_wk, kstar - 1);
+      const bool inq = mem && lane >= first;
+      uint32_t key = 0u;
+      if (inq) {
+        const double *tab = p.prio_table + (size_t)(kstar - 1) * 2 * (B + 1);
+        const float lp = prio_elem_global(tab, p.prio_logEL[kstar - 1], B, lk, wk, sig, -p.prio_b * (double)(Dr - t),
+                                          (float)p.prio_b);
+        key = lp != lp ? 1u : fkey(lp == 0.0f ? 0.0f : lp);  // p = 0 (-inf) stays poppable: fkey(-inf) > 0
+      }
+      int rank = 0;
+      for (int j = 0; j < wc; ++j) {
+        const uint32_t kj = __shfl_sync(FULL, key, j);
+        rank += (kj > key || (kj == key && j < lane)) ? 1 : 0;
+      }
+      selm = __ballot_sync(FULL, inq && rank < kstar);
+    }
+    if (!ALG1 && wc > 1) {   // warp-uniform
     float lg[BPL];
 #pragma unroll
     for (int b = 0; b < BPL; ++b) lg[b] = 0.f;
@@ -356,18 +408,36 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     const uint32_t mx = __reduce_max_sync(FULL, mem ? __float_as_uint(E) : 0u);
     kstar = (int)__reduce_min_sync(FULL, (mem && __float_as_uint(E) == mx) ? (uint32_t)lane : 32u) + 1;
     }
-    const int mbin = (int)__reduce_max_sync(FULL, lane < kstar ? (uint32_t)tb : 0u);
-    const int64_t dur = (int64_t)p.prof.a[kstar - 1] + (int64_t)p.prof.w[kstar - 1] * mbin;
-    const unsigned fm = __ballot_sync(FULL, lane < kstar && t + dur <= Dr);
+    if (!ALG1) selm = kstar >= 32 ? FULL : ((1u << kstar) - 1u);
+    const bool sel = (selm >> lane) & 1u;
+    const int mbin = (int)__reduce_max_sync(FULL, sel ? (uint32_t)tb : 0u);
+    const int64_t dur = ALG1 ? (int64_t)__shfl_sync(FULL, my_ak, kstar - 1) +
+                                   (int64_t)__shfl_sync(FULL, my_wk, kstar - 1) * mbin
+                             : (int64_t)p.prof.a[kstar - 1] + (int64_t)p.prof.w[kstar - 1] * mbin;
+    const unsigned fm = __ballot_sync(FULL, sel && t + dur <= Dr);
     c_fin += __popc(fm);
     c_late += kstar - __popc(fm);
     c_bat += 1;
     c_busy += dur;
     t += dur;
-    if (p.log && lane == 0) p.log[base + s + ndec] = kstar;
+    if (p.log && lane == 0) p.log[base + s + ndec] = ALG1 ? (int32_t)selm : kstar;
     ++ndec;
     ncarry = wc - kstar;
     carry_off = kstar;
+    if (ALG1 && ncarry > 0) {
+      // the unpopped members stay pending in deadline order: compact in place
+      const int64_t hr = mem ? w_h[lane] : 0;
+      const unsigned km = __ballot_sync(FULL, mem && !sel);
+      __syncwarp();
+      if (mem && !sel) {
+        const int slot = __popc(km & ((1u << lane) - 1u));
+        w_dl[slot] = Dr;
+        w_h[slot] = hr;
+        w_d[slot] = dr;
+        w_tb[slot] = tb;
+      }
+      carry_off = 0;
+    }
     __syncwarp();
   }
   if (lane == 0) {
