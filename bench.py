@@ -168,6 +168,51 @@ def time_oracle_c3(cfg, seconds: float, chunk: int = 64):
     return done, t_or, oracle.max_threads()
 
 
+def time_oracle_configs(replay_scenarios: int = 256):
+    """The oracle on the other §8(d) configs, on all host cores (SURVEY §8(d)
+    "Oracle timing"): C1 brute force + O1, C2 and C4 in full, and a C5 subset
+    spanning every family and bucket (O2, free mode)."""
+    import gen
+    import oracle
+    out = {"host_threads": oracle.max_threads(), "nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            out["cpu_model"] = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), None)
+    except OSError:
+        pass
+    c = gen.config1()
+    q = c.queues
+    t0 = time.perf_counter()
+    oracle.bruteforce(c.fam.counts, c.profile.a, c.profile.w, q.deadline, q.dist, int(q.now[0]))
+    t1 = time.perf_counter()
+    oracle.score(oracle.cdf(c.fam.counts), c.profile.a, c.profile.w, q.offsets, q.deadline, q.dist, q.now)
+    t2 = time.perf_counter()
+    out["C1"] = {"bruteforce_ms": 1e3 * (t1 - t0), "o1_ms": 1e3 * (t2 - t1)}
+    for name, cfg in (("C2", gen.config2()), ("C4", gen.config4())):
+        q = cfg.queues
+        F = oracle.cdf(cfg.fam.counts)
+        t0 = time.perf_counter()
+        oracle.score(F, cfg.profile.a, cfg.profile.w, q.offsets, q.deadline, q.dist, q.now)
+        dt = time.perf_counter() - t0
+        out[name] = {"queues": q.Q, "seconds": dt, "decisions_per_s": q.Q / dt}
+    nb = len(gen.BUCKET_SLO_MULTS)
+    per = max(1, replay_scenarios // (len(gen.C5_FAMILIES) * nb))
+    dec, secs, arrivals = 0, 0.0, 0
+    for fam in gen.C5_FAMILIES:
+        tf = gen.c5_trace_family(fam)
+        gids, bucket, slo = gen.c5_scenarios(tf, per)
+        arr, dist, tb = gen.trace_host(tf, gids, gen.C5_ARRIVALS)
+        off = np.arange(len(gids) + 1, dtype=np.int64) * gen.C5_ARRIVALS
+        t0 = time.perf_counter()
+        r = oracle.replay(oracle.cdf(tf.fam.counts), tf.profile.a, tf.profile.w, off, arr, dist, tb, slo)
+        secs += time.perf_counter() - t0
+        dec += int(r["ties"][:, 0].sum())
+        arrivals += len(arr)
+    out["C5"] = {"scenarios": per * len(gen.C5_FAMILIES) * nb, "arrivals": arrivals, "decisions": dec,
+                 "seconds": secs, "decisions_per_s": dec / secs}
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -295,6 +340,31 @@ def main():
             print(json.dumps(result), flush=True)
         return
 
+    # ---------------- C3 secondary shapes: K = 64, identity row layout ----------------
+    if not args.no_extra:
+        var = {}
+        kk = min(64, cfg.kmax)
+        p64 = orj.LatencyProfile(cfg.profile.a[:kk], cfg.profile.w[:kk])
+        ident = orj.Queues(qs.offsets, qs.deadline, torch.arange(qn.N, dtype=torch.int32, device=dev), qs.now)
+        for vname, pr_, qq, kq in (("C3_k64", p64, qs, kk), ("C3_identity_rows", prof, ident, cfg.kmax)):
+            for _ in range(2):
+                orj.pick_batch(store, pr_, qq, bk, bE, stream)
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(10):
+                orj.pick_batch(store, pr_, qq, bk, bE, stream)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            vms = max_over_ranks(v0.elapsed_time(v1)) / 10
+            vc = int(np.minimum(np.diff(qn.offsets), kq).sum())
+            vb = vc * B * 4 + vc * 12 + (Q + 1) * 8 + Q * 16
+            var[vname] = {"kmax": kq, "ms_per_pick": vms, "decisions_per_s": world * Q / (vms / 1e3),
+                          "candidates_per_s": world * vc / (vms / 1e3),
+                          "hbm_frac_algorithmic": vb / (vms / 1e3) / 1e9 / peak}
+        var["C3_identity_rows"]["note"] = "dist_id = identity (each queue's rows contiguous) instead of the permutation"
+        result["c3_variants"] = var
+        del ident
+
     # ---------------- e2e: host buffers through orloj_pick_batch_host ----------------
     if not args.no_e2e:
         pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()  # noqa: E731
@@ -328,6 +398,7 @@ def main():
         result["cpu_baseline"] = {"value": n / secs, "unit": "decisions/s", "cores": cores, "kind": "oracle",
                                   "sample": f"first {n} C3 queues (256 x 256 bins, kmax 256), fp64 oracle, "
                                             f"{secs:.1f} s on {cores} host threads"}
+        result["oracle_by_config"] = time_oracle_configs()
     else:
         result["cpu_baseline"] = None
 
@@ -361,7 +432,8 @@ def run_other_workloads(args, dev, max_over_ranks, world):
 
     out = {}
     stream = torch.cuda.Stream(dev)
-    for name, cfg, reps in (("C2", gen.config2(), 100), ("C4", gen.config4(), 1)):
+    planner_k = None
+    for name, cfg, reps in (("C2", gen.config2(), 100), ("C4", gen.config4(), 1), ("C4-near", gen.config4(near=True), 1)):
         store = wl.score_store(cfg, dev)
         prof = wl.profile(cfg.profile)
         qs = wl.device_queues(cfg.queues, dev, with_arrival=False)
@@ -396,6 +468,10 @@ def run_other_workloads(args, dev, max_over_ranks, world):
                      "us_per_pick": 1e3 * ms, "decisions_per_s": world * Q / (ms / 1e3),
                      "candidates_per_s": world * cands / (ms / 1e3),
                      "timing": f"{iters} x " + (f"CUDA graph of {reps} picks" if reps > 1 else "1 pick")}
+        if name == "C4":
+            planner_k = bk.cpu().numpy()  # == the constant-latency planner, bit for bit (tests)
+        if name == "C4-near" and planner_k is not None and len(planner_k) == Q:
+            out[name]["agreement_with_planner"] = float((bk.cpu().numpy() == planner_k).mean())
         del store, qs
     torch.cuda.empty_cache()
     out["P1"] = run_priority(dev, max_over_ranks, world)
