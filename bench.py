@@ -475,7 +475,59 @@ def run_other_workloads(args, dev, max_over_ranks, world):
         del store, qs
     torch.cuda.empty_cache()
     out["P1"] = run_priority(dev, max_over_ranks, world)
+    out["C2_model_variants"] = run_model_variants(dev, max_over_ranks, world)
     return out
+
+
+def run_model_variants(dev, max_over_ranks, world):
+    """Scoring-model variants on the C2 shape: 1,024
+    SkipNet-like queues x 64, kmax 32, B 64 (orloj_score_model_batches, one
+    launch per pick, 100 picks per CUDA graph)."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+
+    cfg = gen.config2()
+    store = wl.score_store(cfg, dev)
+    qs = wl.device_queues(cfg.queues, dev, with_arrival=False)
+    prof = wl.profile(cfg.profile)
+    B, Q = cfg.fam.B, cfg.queues.Q
+    m = np.arange(B + 1, dtype=np.int64)
+    logm = np.round(B * (2.0 ** (4.0 * m / B) - 1.0) / 15.0).astype(np.int64)
+    tables = {"eq3": prof.a[:, None] + prof.w[:, None] * m[None, :],
+              "log_grid": prof.a[:, None] + prof.w[:, None] * logm[None, :]}
+    steps = ([-cfg.fam.p99_ticks() // 4, 0, cfg.fam.p99_ticks() // 2], [0.25, 1.0, 1.5])
+    res = {}
+    stream = torch.cuda.Stream(dev)
+    for name, tab, interp, st in (("eq3/edge/1 step", "eq3", False, None), ("eq3/uniform/1 step", "eq3", True, None),
+                                  ("eq3/edge/3 steps", "eq3", False, steps),
+                                  ("log_grid/uniform/3 steps", "log_grid", True, steps)):
+        model = orj.ScoreModel(tables[tab], interpolate=interp, steps=st, device=dev)
+        buf = {"E": torch.empty((Q, model.kmax), dtype=torch.float32, device=dev),
+               "best_k": torch.empty(Q, dtype=torch.int32, device=dev),
+               "best_E": torch.empty(Q, dtype=torch.float32, device=dev)}
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                model.score(store, qs, stream, buf)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(100):
+                model.score(store, qs, stream, buf)
+        with torch.cuda.stream(stream):
+            g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1)) / 1000
+        res[name] = {"us_per_pick": 1e3 * ms, "decisions_per_s": world * Q / (ms / 1e3)}
+    del store, qs
+    return res
 
 
 def run_priority(dev, max_over_ranks, world):

@@ -316,6 +316,38 @@ orloj_status orloj_pop_batch(const orloj_queues *queues, const float *log_priori
                              const int32_t *batch_size, int32_t *selected, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Scoring-model variants: the expected finish count
+ *   E_k = sum_{r<=k} sum_s dc_s P(t + L_{B_k} <= D_r + offset_s)
+ * for k = 1..K (K = min(n_q, kmax), kmax <= 32, B <= 128) with
+ *   - duration_ticks: device int64 [kmax][B+1]; dur[k-1][m] = duration of a
+ *     batch of k whose slowest member sits at bin position m (m = 0..B; bin i
+ *     spans positions (i-1, i]); non-decreasing in m (Eq. 3 is a_k + w_k m;
+ *     any grid, e.g. log-spaced, is a table);
+ *   - interpolate = 0: every bin's mass at its upper edge (A1): P = G_k(i*),
+ *     i* = #{m >= 1 : dur[k-1][m] <= x};  interpolate = 1: each member's
+ *     position uniform within its bin (linear CDF inside bins) and
+ *     the duration linear between grid positions: with dur[m] <= x < dur[m+1],
+ *     u = (x - dur[m]) / (dur[m+1] - dur[m]),
+ *     P = prod_j (F_j(m) + u (F_j(m+1) - F_j(m))), F_j(0) = 0; x >= dur[B] -> 1;
+ *   - a piecewise-step cost: num_steps (0 = one unit step at
+ *     offset 0, else 1..8) host arrays step_offset_ticks (strictly increasing)
+ *     and step_cost (cumulative, strictly increasing from > 0); dc_s = c_s - c_{s-1}.
+ * expected_finish: device float [Q][kmax] (entries k > K are 0); best_k /
+ * best_expected: device [Q] or NULL (argmax, ties -> smallest k; 0 for empty
+ * queues).  Async. */
+typedef struct {
+  int32_t kmax;
+  const int64_t *duration_ticks;
+  int32_t interpolate;
+  int32_t num_steps;
+  const int64_t *step_offset_ticks;
+  const double *step_cost;
+} orloj_score_model;
+orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_queues *queues,
+                                       const orloj_score_model *model, float *expected_finish, int32_t *best_k,
+                                       float *best_expected, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Validation (synchronous, O(N), not hot; may allocate a few bytes of scratch).
  * ------------------------------------------------------------------------- */
 /* rows non-decreasing, <= 0, no NaN, [d][B-1] == 0.0f.  INVALID_ARGUMENT otherwise. */

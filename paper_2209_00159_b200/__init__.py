@@ -290,6 +290,57 @@ class PriorityTable:
         return sel
 
 
+class ScoreModel:
+    """Scoring-model variant (orloj_score_model_batches):
+    a duration table dur[k-1][m] (m = 0..B) instead of the Eq. 3 profile,
+    upper-edge or within-bin-uniform bins, and a piecewise-step cost (weighted
+    finish count).  kmax <= 32, B <= 128."""
+
+    def __init__(self, duration_ticks, interpolate: bool = False, steps=None, device="cuda"):
+        dur = np.ascontiguousarray(duration_ticks, dtype=np.int64)
+        if dur.ndim != 2 or not 1 <= dur.shape[0] <= 32:
+            raise OrlojError(1, "duration table must be [kmax <= 32, B+1]")
+        if (np.diff(dur, axis=1) < 0).any():
+            raise OrlojError(1, "duration table must be non-decreasing in the bin position")
+        self.kmax, self.num_bins = dur.shape[0], dur.shape[1] - 1
+        self.dur_host = dur
+        self.dur = torch.from_numpy(dur).to(device)
+        self.interpolate = bool(interpolate)
+        if steps is None:
+            self.off = np.zeros(0, np.int64)
+            self.cost = np.zeros(0, np.float64)
+        else:
+            self.off = np.ascontiguousarray(steps[0], dtype=np.int64)
+            self.cost = np.ascontiguousarray(steps[1], dtype=np.float64)
+            if self.off.shape != self.cost.shape or self.off.ndim != 1:
+                raise OrlojError(1, "steps: offsets and costs must be 1-D of equal length")
+
+    @classmethod
+    def eq3(cls, profile: "LatencyProfile", num_bins: int, **kw) -> "ScoreModel":
+        """The main scorer's model: dur[k-1][m] = a_k + w_k m."""
+        m = np.arange(num_bins + 1, dtype=np.int64)
+        return cls(profile.a[:, None] + profile.w[:, None] * m[None, :], **kw)
+
+    def c(self):
+        self._c = _abi.ScoreModelC(self.kmax, self.dur.data_ptr(), int(self.interpolate), len(self.off),
+                                   self.off.ctypes.data if len(self.off) else None,
+                                   self.cost.ctypes.data if len(self.cost) else None)
+        return ctypes.byref(self._c)
+
+    def score(self, store: HistogramStore, queues: Queues, stream=None, out: Optional[dict] = None) -> dict:
+        """E [Q][kmax], best_k [Q], best_E [Q].  Async on `stream`."""
+        if store.num_bins != self.num_bins:
+            raise OrlojError(1, "duration table and store disagree on B")
+        Q, dev = queues.num_queues, queues.now.device
+        out = out or {}
+        E = out.get("E") if out.get("E") is not None else torch.empty((Q, self.kmax), dtype=torch.float32, device=dev)
+        bk = out.get("best_k") if out.get("best_k") is not None else torch.empty(Q, dtype=torch.int32, device=dev)
+        bE = out.get("best_E") if out.get("best_E") is not None else torch.empty(Q, dtype=torch.float32, device=dev)
+        _abi.check(_abi.lib().orloj_score_model_batches(store.c(), queues.c(), self.c(), E.data_ptr(), bk.data_ptr(),
+                                                        bE.data_ptr(), _stream_ptr(stream)))
+        return {"E": E, "best_k": bk, "best_E": bE}
+
+
 class HostPicker:
     """End-to-end pick for queues in pinned host memory (orloj_pick_batch_host).
 

@@ -67,6 +67,11 @@ class CostSteps(ctypes.Structure):
     _fields_ = [("num_steps", ctypes.c_int32), ("offset_ticks", ctypes.c_void_p), ("cost", ctypes.c_void_p)]
 
 
+class ScoreModelC(ctypes.Structure):
+    _fields_ = [("kmax", ctypes.c_int32), ("duration_ticks", ctypes.c_void_p), ("interpolate", ctypes.c_int32),
+                ("num_steps", ctypes.c_int32), ("step_offset_ticks", ctypes.c_void_p), ("step_cost", ctypes.c_void_p)]
+
+
 class Counters(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("total", "finished", "dropped", "late", "batches", "busy_ticks", "span_ticks")]
@@ -89,6 +94,8 @@ SIGNATURES = {
                                           ctypes.POINTER(TraceC), _P, _P, _P]),
     "orloj_replay_trace_ex": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
                                              ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC), _P, _P, _P]),
+    "orloj_score_model_batches": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC),
+                                                 ctypes.POINTER(ScoreModelC), _P, _P, _P, _P]),
     "orloj_priority_table": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,
                                             _P, ctypes.c_double, _P, _P, _P]),
     "orloj_priority_scores": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "replay_kernel.cuh"
 #include "score_kernel.cuh"
+#include "model_kernel.cuh"
 #include "priority_kernel.cuh"
 #include "store_kernel.cuh"
 
@@ -455,6 +456,69 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "replay_trace launch");
+  return ok();
+}
+
+orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_queues *queues,
+                                       const orloj_score_model *model, float *E, int32_t *best_k, float *best_E,
+                                       void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, MODEL_MAX_BINS))) return st;
+  if ((st = check_queues(queues))) return st;
+  if (!model || model->kmax < 1 || model->kmax > 32 || !model->duration_ticks ||
+      (model->interpolate != 0 && model->interpolate != 1))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "score model: need 1 <= kmax <= 32, a duration table, interpolate 0/1");
+  ModelParams p;
+  std::memset(&p, 0, sizeof(p));
+  if (model->num_steps == 0) {
+    p.nsteps = 1;
+    p.off[0] = 0;
+    p.dc[0] = 1.f;
+  } else {
+    if (model->num_steps < 0 || model->num_steps > MODEL_MAX_STEPS || !model->step_offset_ticks || !model->step_cost)
+      return fail(ORLOJ_ERR_INVALID_ARGUMENT, "score model: 0..%d steps with both arrays", MODEL_MAX_STEPS);
+    double prev = 0.0;
+    for (int i = 0; i < model->num_steps; ++i) {
+      const int64_t o = model->step_offset_ticks[i];
+      const double dc = model->step_cost[i] - prev;
+      if ((i > 0 && o <= model->step_offset_ticks[i - 1]) || o < -(1ll << 40) || o > (1ll << 40) || !(dc > 0.0))
+        return fail(ORLOJ_ERR_INVALID_ARGUMENT,
+                    "score model steps: offsets must increase (|offset| <= 2^40), costs strictly increase from 0");
+      p.off[i] = o;
+      p.dc[i] = (float)dc;
+      prev = model->step_cost[i];
+    }
+    p.nsteps = model->num_steps;
+  }
+  if (queues->num_queues == 0) return ok();
+  if (!E) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "score model: expected_finish is NULL");
+  p.log2F = store->log2_cdf;
+  p.D = store->num_dists;
+  p.B = store->num_bins;
+  p.kmax = model->kmax;
+  p.Q = queues->num_queues;
+  p.offsets = queues->queue_offsets;
+  p.deadline = queues->deadline_ticks;
+  p.now = queues->now_ticks;
+  p.dist = queues->dist_id;
+  p.dur = model->duration_ticks;
+  p.E = E;
+  p.best_k = best_k;
+  p.best_E = best_E;
+  p.smem_store = (int64_t)p.D * p.B * 4 <= (32 << 10);
+  const size_t smem = model_smem_bytes(p.kmax, p.B, p.D, p.smem_store);
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)((p.Q + MODEL_WARPS - 1) / MODEL_WARPS);
+  cudaError_t e;
+  if (model->interpolate) {
+    e = cudaFuncSetAttribute(model_score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) model_score_kernel<true><<<grid, MODEL_WARPS * 32, smem, s>>>(p);
+  } else {
+    e = cudaFuncSetAttribute(model_score_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) model_score_kernel<false><<<grid, MODEL_WARPS * 32, smem, s>>>(p);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "score_model launch");
   return ok();
 }
 
