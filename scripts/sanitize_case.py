@@ -32,6 +32,23 @@ def main():
     f = wl.C5Family("skipnet", local_ids=np.arange(8), n_arr=500)
     f.trace.validate(f.store)
     orj.replay_trace(f.store, f.profile, f.trace, decision_log=True)
+    orj.replay_trace(f.store, f.profile, f.trace, objective="finish_rate")
+    # Alg. 1 policy (priority tables inside the replay kernel)
+    from paper_2209_00159_b200 import policy
+    pt = orj.PriorityTable(f.store, f.profile, f.profile.kmax, 1.0 / f.tf.fam.mean_ticks())
+    thr = torch.from_numpy(policy.alg1_size_thresholds(f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).cuda()
+    orj.replay_trace(f.store, f.profile, f.trace, decision_log=True, objective="alg1", priority=pt,
+                     size_thresholds=thr)
+    # priorities (+ steps), PopBatch, model variants, profiler on the C1 queue
+    tab = orj.PriorityTable(st, pr, 4, 1e-3)
+    lp = tab.scores(q)
+    tab.scores(q, steps=([0, 500], [1.0, 2.0]))
+    tab.pop(q, lp, torch.tensor([3], dtype=torch.int32, device="cuda"))
+    for interp in (False, True):
+        orj.ScoreModel.eq3(pr, st.num_bins, interpolate=interp, steps=([0, 300], [1.0, 1.5])).score(st, q)
+    prof = orj.Profiler(st.num_dists, st.num_bins, st.bin_ticks)
+    prof.add(torch.tensor([0, 1, 2], dtype=torch.int32, device="cuda"),
+             torch.tensor([5, 1500, 99999], dtype=torch.int64, device="cuda"))
     torch.cuda.synchronize()
     print("sanitize case OK")
 
