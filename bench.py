@@ -53,6 +53,12 @@ def parse():
     ap.add_argument("--replay-seeds", type=int, default=256, help="seeds per (family, bucket)")
     ap.add_argument("--replay-arrivals", type=int, default=100_000)
     ap.add_argument("--replay-reps", type=int, default=2)
+    ap.add_argument("--replay-segments", default="auto",
+                    help="segments per scenario of the segmented replay ('auto' or an int; 1 = plain kernel)")
+    ap.add_argument("--seg-sweep-n", default="1,2,4,8")
+    ap.add_argument("--seg-sweep-g", default="1,2,4,8,16,32,64,auto")
+    ap.add_argument("--replay-seg-sweep", action="store_true",
+                    help="diagnostic: time the C5 sweep and its rank-0 shards for several segment counts")
     ap.add_argument("--no-shard-proxy", action="store_true")
     ap.add_argument("--no-policies", action="store_true", help="skip the replay policy-variant sweep")
     ap.add_argument("--policy-seeds", type=int, default=32)
@@ -274,6 +280,20 @@ def main():
         tt = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
+
+    if args.replay_seg_sweep:
+        out = {}
+        for N in [int(x) for x in args.seg_sweep_n.split(",")]:
+            sf = build_replay(args, 0, N, dev)
+            for G in args.seg_sweep_g.split(","):
+                ms, tabs, _ = time_replay(sf, args.replay_reps, dev, lambda: None, lambda x: x, reduce=False,
+                                          segments=G)
+                out[f"N{N}/G{G}"] = {"ms": round(ms, 3), "segments": list(time_replay.segments),
+                                     "decisions": int(tabs[:, :, 4].sum()), "stitch": time_replay.stats}
+                print(json.dumps({f"N{N}/G{G}": out[f"N{N}/G{G}"]}), flush=True)
+            del sf
+        print(json.dumps({"replay_seg_sweep": out}), flush=True)
+        return
 
     if args.only_replay:
         r = run_replay(args, rank, world, dev, barrier, max_over_ranks)
@@ -597,7 +617,18 @@ def build_replay(args, rank, world, dev):
                         device=dev) for name in gen.C5_FAMILIES]
 
 
-def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True):
+def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
+    """Segments per scenario for the segmented replay.  "auto": 8 per scenario
+    while a family has >= 1,024 scenarios on this rank, else 16 (the C5 sweep's
+    measured optimum at 1/2/4/8-GPU shard sizes), never below
+    ~2,000 arrivals per segment."""
+    if spec != "auto":
+        return max(1, int(spec))
+    g = 8 if n_scen_family >= 1024 else 16
+    return int(max(1, min(g, n_arr // 2000, 4096)))
+
+
+def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True, segments="auto"):
     """One sweep = the 4 family replays on 4 streams + one all-reduce of the
     [4 x 8 x 7] int64 counters (NCCL; a no-op on one rank), all inside the
     timed region.  Returns (ms per sweep, counters [4, 8, 7], clock summary)."""
@@ -611,14 +642,18 @@ def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True):
     streams = [torch.cuda.Stream(dev) for _ in fams]
     main = torch.cuda.current_stream()
     tables = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
+    segs = [replay_segments(segments, f.trace.num_scenarios, f.trace.num_arrivals // max(f.trace.num_scenarios, 1))
+            for f in fams]
+    wss = [torch.empty(max(orj.replay_seg_workspace_bytes(f.trace, g), 1), dtype=torch.uint8, device=dev)
+           for f, g in zip(fams, segs)]   # allocated once, outside the timed region
 
     def once():
         tables.zero_()
         start = torch.cuda.Event()
         start.record(main)
-        for f, s, t_ in zip(fams, streams, tables):
+        for f, s, t_, g, ws in zip(fams, streams, tables, segs, wss):
             s.wait_event(start)
-            orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, stream=s)
+            orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, stream=s, segments=g, workspace=ws)
         for s in streams:
             ev = torch.cuda.Event()
             ev.record(s)
@@ -637,6 +672,8 @@ def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True):
         e1.record(main)
         torch.cuda.synchronize()
     barrier()
+    time_replay.segments = segs
+    time_replay.stats = [orj.replay_seg_stats(ws) if g > 1 else None for ws, g in zip(wss, segs)]
     return max_over_ranks(e0.elapsed_time(e1)) / reps, tables.cpu().numpy(), clk.summary()
 
 
@@ -705,7 +742,10 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
     import gen
 
     fams = build_replay(args, rank, world, dev)
-    ms, tabs, clk = time_replay(fams, args.replay_reps, dev, barrier, max_over_ranks)
+    ms, tabs, clk = time_replay(fams, args.replay_reps, dev, barrier, max_over_ranks,
+                                segments=args.replay_segments)
+    segs = list(time_replay.segments)
+    stitch = list(time_replay.stats)
     per_family = {f.tf.fam.name: t_ for f, t_ in zip(fams, tabs)}
     tot = tabs.sum(0)
     decisions = int(tot[:, 4].sum())
@@ -718,7 +758,10 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
            "value": decisions / (ms / 1e3), "unit": "decisions/s", "arrivals_per_s": arrivals / (ms / 1e3),
            "ms_per_sweep": ms, "decisions": decisions, "arrivals": arrivals, "scaling": "strong",
            "finish_rate_by_bucket": fr, "slo_multipliers": list(gen.BUCKET_SLO_MULTS), "utilisation": util,
-           "gpu_launches_per_sweep": len(fams), "clocks": clk,
+           "segments_per_scenario": segs, "stitch_stats": stitch,
+           "replay_kernel": "segmented (orloj_replay_trace_seg: speculative segments + stitch, 2 launches per family)"
+                            if max(segs) > 1 else "plain (one warp per scenario)",
+           "gpu_launches_per_sweep": sum(2 if g > 1 else 1 for g in segs), "clocks": clk,
            "collective": "one torch.distributed.all_reduce of the int64 [4 x 8 x 7] counters (NCCL) per sweep, "
                          "inside the timed region"}
     if not args.no_policies:
@@ -730,8 +773,10 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
         proxy = {}
         for N in (2, 4, 8):
             sf = build_replay(args, 0, N, dev)
-            sms, _, _ = time_replay(sf, 1, dev, lambda: None, lambda x: x, reduce=False)
-            proxy[str(N)] = {"ms_rank0_shard": sms, "implied_speedup": ms / sms}
+            sms, stabs, _ = time_replay(sf, 1, dev, lambda: None, lambda x: x, reduce=False,
+                                        segments=args.replay_segments)
+            proxy[str(N)] = {"ms_rank0_shard": sms, "implied_speedup": ms / sms,
+                             "segments_per_scenario": list(time_replay.segments)}
             del sf
         out["shard_proxy"] = proxy
     return out

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define ORLOJ_ABI_VERSION 2
+#define ORLOJ_ABI_VERSION 3
 #define ORLOJ_MAX_KMAX 256        /* candidate batch sizes per queue (score / pick) */
 #define ORLOJ_MAX_BINS 256        /* bins per histogram (score / pick) */
 #define ORLOJ_REPLAY_MAX_KMAX 32  /* window size in replay */
@@ -252,6 +252,39 @@ typedef struct {
 orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency_profile *profile,
                                    const orloj_trace *trace, const orloj_replay_policy *policy,
                                    orloj_counters *per_bucket, int32_t *decision_log, void *stream);
+
+/* Segmented replay: the same replay (every counter and decision-log entry
+ * identical to orloj_replay_trace_ex, bit for bit) with a shorter critical
+ * path.  Each scenario's arrivals are cut into `segments` equal ranges
+ * s_g = floor(g n / segments); one warp per (scenario, segment) replays range g
+ * from an empty queue and records where its run *regenerates* (at a decision
+ * point nothing is pending and the worker is free by the next arrival j: from
+ * there on the run equals a fresh replay started at j, whatever came before);
+ * a second pass continues the true run from segment 0 and, in each later
+ * segment, switches to the segment's own run at the first regeneration point
+ * both pass through (or runs through the segment itself when there is none).
+ * The scenarios' sequential decision chains (A9, A15: one worker, non-
+ * preemptive) are what bounds the replay on many SMs; segments split them.
+ * segments: 1..ORLOJ_REPLAY_MAX_SEGMENTS (1 = orloj_replay_trace_ex; workspace
+ * may then be NULL).  num_arrivals: arrival_offsets[S] (sizes the workspace).
+ * workspace: caller-owned, 256-byte aligned device memory of at least
+ * orloj_replay_seg_workspace(S, num_arrivals, segments, decision_log != NULL)
+ * bytes; contents are scratch except its first 32 bytes, which hold int64
+ * diagnostics of the call once it completes: {decisions the second pass re-ran,
+ * segments joined at a common regeneration point, segments run through,
+ * decisions the first pass made past the segment ends}.
+ * policy: as orloj_replay_trace_ex (NULL: the
+ * default expected-finish policy).  Errors: INVALID_ARGUMENT for a bad segment
+ * count or a missing / short / misaligned workspace, else as
+ * orloj_replay_trace_ex. */
+#define ORLOJ_REPLAY_MAX_SEGMENTS 4096
+size_t orloj_replay_seg_workspace(int64_t num_scenarios, int64_t num_arrivals, int32_t segments,
+                                  int32_t with_log);
+orloj_status orloj_replay_trace_seg(const orloj_store *store, const orloj_latency_profile *profile,
+                                    const orloj_trace *trace, const orloj_replay_policy *policy,
+                                    int32_t segments, int64_t num_arrivals, void *workspace,
+                                    size_t workspace_bytes, orloj_counters *per_bucket,
+                                    int32_t *decision_log, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Eq. 1-2 priority scores and PopBatch (PAPER.md:423-455,

@@ -449,7 +449,8 @@ OBJECTIVES = {"expected_finish": 0, "finish_rate": 1, "alg1": 2}
 def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, per_bucket=None,
                  decision_log: bool | torch.Tensor = False, stream=None, objective: str = "expected_finish",
                  drop_threshold: Optional[torch.Tensor] = None, priority: Optional["PriorityTable"] = None,
-                 size_thresholds: Optional[torch.Tensor] = None):
+                 size_thresholds: Optional[torch.Tensor] = None, segments: int = 1,
+                 workspace: Optional[torch.Tensor] = None):
     """Replay every scenario; returns (per_bucket int64 [num_buckets, 7], log or None).
     per_bucket is ADDED to (pass a zeroed tensor to accumulate across calls).
     objective: "expected_finish" (argmax E_k) or "finish_rate" (argmax
@@ -458,7 +459,10 @@ def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, p
     objective "alg1" (the paper's Alg. 1 iteration, include/orloj.h) needs
     `priority` (a PriorityTable with num_sizes = kmax) and `size_thresholds`
     (device int64 [kmax], policy.alg1_size_thresholds); the decision log then
-    holds popped-member bit masks."""
+    holds popped-member bit masks.
+    segments > 1: the exact segmented replay (orloj_replay_trace_seg; same
+    counters and log, shorter critical path); `workspace` (uint8 device tensor
+    of replay_seg_workspace_bytes(...) bytes) is allocated when not given."""
     dev = trace.arrival.device
     if per_bucket is None:
         per_bucket = torch.zeros((trace.num_buckets, 7), dtype=torch.int64, device=dev)
@@ -487,6 +491,27 @@ def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, p
         pol.priority_table = priority.log_table.data_ptr()
         pol.priority_log_expected = priority.log_expected.data_ptr()
         pol.priority_b_per_tick = priority.b
-    _abi.check(_abi.lib().orloj_replay_trace_ex(store.c(), profile.c(), trace.c(), ctypes.byref(pol),
-                                                per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
+    if segments == 1:
+        _abi.check(_abi.lib().orloj_replay_trace_ex(store.c(), profile.c(), trace.c(), ctypes.byref(pol),
+                                                    per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
+        return per_bucket, log
+    need = replay_seg_workspace_bytes(trace, segments, log is not None)
+    if workspace is None:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    _dev(workspace, torch.uint8, "workspace")
+    _abi.check(_abi.lib().orloj_replay_trace_seg(store.c(), profile.c(), trace.c(), ctypes.byref(pol), int(segments),
+                                                 trace.num_arrivals, _ptr(workspace), workspace.numel(),
+                                                 per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
     return per_bucket, log
+
+
+def replay_seg_stats(workspace: torch.Tensor) -> dict:
+    """Diagnostics a completed segmented replay left in its workspace head."""
+    v = workspace[:32].view(torch.int64).cpu().tolist()
+    return {"stitch_decisions": v[0], "joined": v[1], "crossed": v[2], "extension_decisions": v[3]}
+
+
+def replay_seg_workspace_bytes(trace: Trace, segments: int, with_log: bool = False) -> int:
+    """Device workspace of the segmented replay (orloj_replay_seg_workspace)."""
+    return int(_abi.lib().orloj_replay_seg_workspace(trace.num_scenarios, trace.num_arrivals, int(segments),
+                                                     int(bool(with_log))))

@@ -27,13 +27,37 @@ class OrlojError(RuntimeError):
         self.status = status
 
 
-def build(nvcc: str = "nvcc", verbose: bool = False) -> str:
-    src = os.path.join(PKG, "csrc", "orloj.cu")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, src]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
-    return LIB_PATH
+def build(nvcc: str = "nvcc", verbose: bool = False, out: str | None = None, defines=(), only=None) -> str:
+    """Compile every csrc/*.cu translation unit for sm_100a in parallel and link
+    liborloj.so (each TU's kernels are launched only from that TU: no
+    relocatable device code).  out / defines: a variant library built with
+    extra -D flags (loaded through ORLOJ_LIB) for experiments; only: rebuild
+    just these TUs (the other objects are reused)."""
+    from concurrent.futures import ThreadPoolExecutor
+    csrc = os.path.join(PKG, "csrc")
+    out = out or LIB_PATH
+    objdir = os.path.join(PKG, "build", os.path.basename(out).replace(".so", ""))
+    os.makedirs(objdir, exist_ok=True)
+    srcs = sorted(f for f in os.listdir(csrc) if f.endswith(".cu"))
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
+
+    def one(f):
+        obj = os.path.join(objdir, f[:-3] + ".o")
+        if only is not None and f not in only and os.path.exists(obj):
+            return obj
+        cmd = [nvcc, *compile_flags, "-c", "-o", obj, os.path.join(csrc, f)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(one, srcs))
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    tmp = out + ".tmp"
+    subprocess.check_call([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs])
+    os.replace(tmp, out)
+    return out
 
 
 class Store(ctypes.Structure):
@@ -94,6 +118,11 @@ SIGNATURES = {
                                           ctypes.POINTER(TraceC), _P, _P, _P]),
     "orloj_replay_trace_ex": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
                                              ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC), _P, _P, _P]),
+    "orloj_replay_seg_workspace": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                                     ctypes.c_int32]),
+    "orloj_replay_trace_seg": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                              ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC), ctypes.c_int32,
+                                              ctypes.c_int64, _P, ctypes.c_size_t, _P, _P, _P]),
     "orloj_score_model_batches": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC),
                                                  ctypes.POINTER(ScoreModelC), _P, _P, _P, _P]),
     "orloj_priority_table": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,

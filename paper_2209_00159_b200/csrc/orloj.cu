@@ -15,7 +15,8 @@
 #include <string>
 
 #include "common.cuh"
-#include "replay_kernel.cuh"
+#include "host_util.h"
+#include "score_launch.cuh"
 #include "score_kernel.cuh"
 #include "model_kernel.cuh"
 #include "priority_kernel.cuh"
@@ -23,7 +24,8 @@
 
 using namespace orloj;
 
-namespace {
+namespace orloj {
+namespace host {
 
 thread_local std::string g_last_error;
 
@@ -107,63 +109,18 @@ int slots_for(int kmax) {
   return c <= 1 ? 1 : c <= 2 ? 2 : c <= 4 ? 4 : 8;
 }
 
-// Row source of the score kernel: TMA ring from HBM (STREAM adds L1 bypass and
-// L2 evict-first for stores larger than L2), or the whole store staged in
-// shared memory when it is small (a few application histograms).
-enum class RowSrc { Tma, TmaStream, Smem };
-constexpr int64_t STREAM_STORE_BYTES = 256ll << 20;
-constexpr int64_t SMEM_STORE_BYTES = 48ll << 10;
+}  // namespace host
+}  // namespace orloj
 
-template <int BPL, int SLOTS, bool PICK, bool STREAM, bool SMEMS>
-cudaError_t launch_score_t(const ScoreParams &p, cudaStream_t s) {
-  const int64_t blocks = (p.Q + SCORE_WARPS - 1) / SCORE_WARPS;
-  const size_t base = ScoreShape<BPL>::smem_bytes();
-  const size_t smem = base + (SMEMS ? (size_t)p.D * p.B * 4 : 0);
-  const size_t cap = base + (SMEMS ? (size_t)SMEM_STORE_BYTES : 0);
-  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
-  if (!configured.load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_release);
-  }
-  score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS><<<(unsigned)blocks, SCORE_WARPS * 32, smem, s>>>(p);
-  return cudaGetLastError();
-}
+using namespace orloj::host;
 
-template <int BPL, bool PICK, bool STREAM, bool SMEMS>
-cudaError_t launch_score_s(const ScoreParams &p, cudaStream_t s) {
-  switch (slots_for(p.kmax)) {
-    case 1: return launch_score_t<BPL, 1, PICK, STREAM, SMEMS>(p, s);
-    case 2: return launch_score_t<BPL, 2, PICK, STREAM, SMEMS>(p, s);
-    case 4: return launch_score_t<BPL, 4, PICK, STREAM, SMEMS>(p, s);
-    default: return launch_score_t<BPL, 8, PICK, STREAM, SMEMS>(p, s);
-  }
-}
-
-template <int BPL, bool PICK>
-cudaError_t launch_score_r(const ScoreParams &p, RowSrc src, cudaStream_t s) {
-  if (src == RowSrc::Smem) return launch_score_s<BPL, PICK, false, true>(p, s);
-  if constexpr (BPL == 8)
-    if (src == RowSrc::TmaStream) return launch_score_s<8, PICK, true, false>(p, s);
-  return launch_score_s<BPL, PICK, false, false>(p, s);
-}
-
-template <bool PICK>
-cudaError_t launch_score_b(const ScoreParams &p, RowSrc src, cudaStream_t s) {
-  switch (bins_per_lane(p.B)) {
-    case 1: return launch_score_r<1, PICK>(p, src, s);
-    case 2: return launch_score_r<2, PICK>(p, src, s);
-    case 4: return launch_score_r<4, PICK>(p, src, s);
-    default: return launch_score_r<8, PICK>(p, src, s);
-  }
-}
+namespace {
 
 cudaError_t launch_score(const ScoreParams &p, bool pick, int64_t store_bytes, cudaStream_t s) {
   const RowSrc src = store_bytes <= SMEM_STORE_BYTES ? RowSrc::Smem
                      : store_bytes > STREAM_STORE_BYTES ? RowSrc::TmaStream
                                                         : RowSrc::Tma;
-  return pick ? launch_score_b<true>(p, src, s) : launch_score_b<false>(p, src, s);
+  return pick ? launch_score_pick(p, src, s) : launch_score_all(p, src, s);
 }
 
 orloj_status prepare_score(const orloj_store *store, const orloj_latency_profile *profile,
@@ -369,93 +326,6 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
     if (e == cudaSuccess) e = cudaMemcpyAsync(bE_h, bE_d, Q * 4, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(e, "pick_batch_host D2H");
   }
-  return ok();
-}
-
-orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
-                                const orloj_trace *tr, orloj_counters *per_bucket, int32_t *log, void *stream) {
-  const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
-  return orloj_replay_trace_ex(store, profile, tr, &def, per_bucket, log, stream);
-}
-
-orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency_profile *profile,
-                                   const orloj_trace *tr, const orloj_replay_policy *policy,
-                                   orloj_counters *per_bucket, int32_t *log, void *stream) {
-  orloj_status st;
-  if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
-  if (!policy || (policy->objective != ORLOJ_OBJ_EXPECTED_FINISH && policy->objective != ORLOJ_OBJ_FINISH_RATE &&
-                  policy->objective != ORLOJ_OBJ_ALG1))
-    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay policy: objective must be EXPECTED_FINISH, FINISH_RATE or ALG1");
-  const bool rate = policy->objective == ORLOJ_OBJ_FINISH_RATE;
-  const bool alg1 = policy->objective == ORLOJ_OBJ_ALG1;
-  if (alg1 && (!policy->size_threshold_ticks || !policy->priority_table || !policy->priority_log_expected ||
-               !(policy->priority_b_per_tick > 0.0) || policy->drop_threshold_ticks))
-    return fail(ORLOJ_ERR_INVALID_ARGUMENT,
-                "replay policy ALG1: needs size thresholds, priority tables for sizes 1..kmax and b > 0, "
-                "and no drop thresholds (Alg. 1 drops by the bs = 1 threshold)");
-  if (!tr || tr->num_scenarios < 0 || tr->num_buckets < 1)
-    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace: need num_scenarios >= 0 and num_buckets >= 1");
-  if (tr->num_scenarios > 0 && (!tr->arrival_offsets || !tr->arrival_ticks || !tr->dist_id || !tr->true_bin ||
-                                !tr->slo_ticks || !tr->bucket || !per_bucket))
-    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace arrays / per_bucket must be non-NULL device pointers");
-  ReplayParams p;
-  std::memset(&p, 0, sizeof(p));
-  if ((st = compile_profile(profile, store->num_bins, ORLOJ_REPLAY_MAX_KMAX, &p.prof))) return st;
-  const int B = store->num_bins, D = store->num_dists;
-  const int bpl = bins_per_lane(B);
-  const size_t store_b = (size_t)D * B * 4;
-  if (store_b > (64u << 10))
-    return fail(ORLOJ_ERR_CAPACITY, "replay: store of %zu bytes exceeds the 64 KiB shared-memory budget", store_b);
-  const size_t warp_b = rate ? (bpl == 1 ? ReplayWarpSmem<1, true>::bytes()
-                                         : bpl == 2 ? ReplayWarpSmem<2, true>::bytes() : ReplayWarpSmem<4, true>::bytes())
-                             : (bpl == 1 ? ReplayWarpSmem<1>::bytes()
-                                         : bpl == 2 ? ReplayWarpSmem<2>::bytes() : ReplayWarpSmem<4>::bytes());
-  const size_t smem = replay_head_bytes(D, B) + REPLAY_WARPS * warp_b;
-  p.log2F = store->log2_cdf;
-  p.D = D;
-  p.B = B;
-  p.S = tr->num_scenarios;
-  p.arr_off = tr->arrival_offsets;
-  p.arrival = tr->arrival_ticks;
-  p.dist = tr->dist_id;
-  p.true_bin = tr->true_bin;
-  p.slo = tr->slo_ticks;
-  p.bucket = tr->bucket;
-  p.counters = reinterpret_cast<unsigned long long *>(per_bucket);
-  p.log = log;
-  p.drop_thr = policy->drop_threshold_ticks;
-  if (alg1) {
-    p.size_thr = policy->size_threshold_ticks;
-    p.prio_table = policy->priority_table;
-    p.prio_logEL = policy->priority_log_expected;
-    p.prio_b = policy->priority_b_per_tick;
-  }
-  if (p.S == 0) return ok();
-  const unsigned blocks = (unsigned)((p.S + REPLAY_WARPS - 1) / REPLAY_WARPS);
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e;
-  switch (bpl * 4 + (rate ? 1 : 0) + (alg1 ? 2 : 0)) {
-#define ORLOJ_REPLAY_CASE(BPL_, RATE_, ALG1_)                                                                  \
-  case BPL_ * 4 + (RATE_ ? 1 : 0) + (ALG1_ ? 2 : 0):                                                           \
-    e = cudaFuncSetAttribute(replay_kernel<BPL_, RATE_, ALG1_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                             (int)smem);                                                                       \
-    if (e == cudaSuccess) replay_kernel<BPL_, RATE_, ALG1_><<<blocks, REPLAY_WARPS * 32, smem, s>>>(p);        \
-    break;
-    ORLOJ_REPLAY_CASE(1, false, false)
-    ORLOJ_REPLAY_CASE(1, true, false)
-    ORLOJ_REPLAY_CASE(1, false, true)
-    ORLOJ_REPLAY_CASE(2, false, false)
-    ORLOJ_REPLAY_CASE(2, true, false)
-    ORLOJ_REPLAY_CASE(2, false, true)
-    ORLOJ_REPLAY_CASE(4, false, false)
-    ORLOJ_REPLAY_CASE(4, true, false)
-    ORLOJ_REPLAY_CASE(4, false, true)
-#undef ORLOJ_REPLAY_CASE
-    default:
-      return fail(ORLOJ_ERR_CAPACITY, "replay: unsupported bins per lane");
-  }
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "replay_trace launch");
   return ok();
 }
 

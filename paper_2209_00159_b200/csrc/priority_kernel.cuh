@@ -31,7 +31,7 @@ __device__ __forceinline__ uint32_t fkey(float x) {
 // One block per batch size: mixture CDF, pmf of the max of bs draws, E[L],
 // the full-bin prefix C[0..B] and the per-bin log(h_i / b) H[0..B] (H[0] =
 // -inf), all fp64.  table layout [S][2][B+1]: [s][0][i] = C[i], [s][1][i] = H[i].
-__global__ void priority_table_kernel(const float *__restrict__ log2F, int32_t D, int32_t B,
+static __global__ void priority_table_kernel(const float *__restrict__ log2F, int32_t D, int32_t B,
                                       const float *__restrict__ weights, const __grid_constant__ ProfileDev prof,
                                       double b, double *__restrict__ table, double *__restrict__ logEL) {
   extern __shared__ double s_mix[];  // [B]
@@ -243,7 +243,7 @@ __device__ __forceinline__ void cx(uint32_t &ka, int &ia, uint32_t &kb, int &ib)
 // lane holding the best head (REDUX max over keys, then min over member
 // indices among equal keys) pops it.  Round r's winner is kept by lane r and
 // the 32 results leave in one coalesced store.
-__global__ void __launch_bounds__(256) pop_batch_kernel(const float *__restrict__ logp, int32_t S, int64_t Q,
+static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__restrict__ logp, int32_t S, int64_t Q,
                                                         const int64_t *__restrict__ offsets,
                                                         const int32_t *__restrict__ bs_q, int32_t *__restrict__ sel) {
   const int lane = threadIdx.x & 31;

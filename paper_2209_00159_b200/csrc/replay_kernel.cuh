@@ -22,6 +22,26 @@
 //  * argmax by two REDUX (max of float bits, then min k), dispatch with one
 //    more REDUX (max true bin) and one ballot (finished, A11 / late, A17).
 // Counters are kept warp-uniform and added to per-bucket int64 totals at the end.
+//
+// Segmented replay (MODE 1 + MODE 2; exact, DESIGN.md §7 "segments").  A state
+// at a loop top with nothing carried and the worker free by the next arrival j
+// (ncarry == 0, t <= a_j) is a *regeneration point*: the rest of the run is the
+// same as a fresh replay started at arrival j (the max-plus scan and the idle
+// jump both give t'_j = a_j whatever t <= a_j was, and the lookahead, the scan
+// and hence every later decision depend only on (t, cursor, carry)).  MODE 1
+// runs G segments of a scenario in parallel, segment g from a fresh start at
+// s_g = floor(g n / G) until its first loop top with cursor >= s_{g+1} (its
+// end state), recording regeneration points with their prefix counters, and
+// then runs on past s_{g+1} (the extension) recording regeneration points at
+// the marks segment g+1 uses, until a few records after its first one.  MODE 2
+// (one warp per scenario) stitches: the true run starts at segment 0's end
+// state; wherever segment g-1's extension and segment g's records share a
+// regeneration point, the true run is segment g-1 up to that point and segment
+// g after it, so both parts' counters (and decision logs) are taken without
+// re-running anything.  Otherwise the true run is re-run from segment g-1's end
+// state until it reaches one of segment g's recorded regeneration points (or
+// runs through the segment).  The counters and the log are those of the plain
+// replay, bit for bit; only the critical path gets shorter.
 #pragma once
 #include "common.cuh"
 #include "priority_kernel.cuh"
@@ -49,7 +69,55 @@ struct ReplayParams {
   const double *prio_logEL;
   double prio_b;
   ProfileDev prof;
+  // segmented replay (MODE 1 / 2)
+  int32_t G;                      // segments per scenario
+  struct ReplaySeg *seg;          // [S][G]
+  int32_t *seg_log;               // scratch decision logs of segments g >= 1 (MODE 1 with a log)
+  unsigned long long *seg_stats;  // [4]: decisions re-run by the stitch, segments joined, segments crossed,
+                                  //      decisions in the extensions
 };
+
+constexpr int SEG_REC = 20;  // regeneration points recorded per list
+// Records sit at marks m_0 = 0, m_{k+1} = m_k + max(8, m_k / 2) arrivals past
+// the list's base: a record is the first regeneration point at or past the next
+// mark.  A segment run starts empty and regenerates often at first while the
+// true run may still be clearing a backlog; marks spaced geometrically keep a
+// record within ~1.5x of wherever the true run regenerates, and two runs that
+// have become the same run record the same points from the next mark on.
+__host__ __device__ inline int64_t seg_next_mark(int64_t m) { return m + (m / 2 > 8 ? m / 2 : 8); }
+// the extension past s_{g+1} stops after its first regeneration point and this many more records
+#ifndef ORLOJ_SEG_EXT_AFTER
+#define ORLOJ_SEG_EXT_AFTER 1
+#endif
+constexpr int SEG_EXT_AFTER = ORLOJ_SEG_EXT_AFTER;
+// a regeneration point: arrival index, decisions and counters {finished,
+// dropped, late, batches, busy} of the recording run before that point
+struct SegRec {
+  long long j, ndec, ctr[5];
+};
+struct ReplaySeg {
+  int64_t t, cursor, ndec;  // end state of the segment run (first loop top with cursor >= s_{g+1})
+  long long ctr[5];
+  int32_t ncarry, nrec, next, pad;
+  SegRec rec[SEG_REC];  // the run's regeneration points in [s_g, s_{g+1}) (marks from s_g)
+  SegRec ext[SEG_REC];  // its extension past the end state (marks from s_{g+1}; running counters)
+  int64_t carry_D[32], carry_h[32];
+  int32_t carry_d[32], carry_tb[32];
+};
+
+// first arrival of segment g of G over n arrivals: floor(g n / G) without overflow
+__host__ __device__ inline int64_t seg_begin(int64_t n, int g, int G) {
+  return g >= G ? n : (n / G) * g + (n % G) * g / G;
+}
+// start of segment (s, g)'s scratch decision log.  The run of segment g with
+// its extension (capped at s_{g+2}) makes at most (s_{g+2} - s_g) + 32
+// decisions (members are dispatched once each; only the last iteration
+// consumes arrivals past the cap, at most kmax <= 32 kept), so the regions
+// [off_g, off_g + s_{g+2} - s_g + 34) are disjoint: per scenario 2n + 34 G
+// entries, 2N + 34 S G in all.
+__host__ __device__ inline int64_t seg_log_off(int64_t arr_off_s, int64_t s, int64_t n, int g, int G) {
+  return 2 * arr_off_s + seg_begin(n, g, G) + seg_begin(n, g + 1, G) - seg_begin(n, 1, G) + (s * G + g) * 34;
+}
 
 constexpr int REPLAY_WARPS = 4;
 #ifndef ORLOJ_REPLAY_KB
@@ -66,7 +134,7 @@ struct ReplayWarpSmem {
   static constexpr int STG = 32 * BPL + 4;
   static constexpr int PSTRIDE = 36;
   static constexpr size_t BYTES = (size_t)(REPLAY_KB * STG) * 4 + 32 * (8 + 8 + 4 + 4) +
-                                  (RATE ? 2 : 1) * 32 * PSTRIDE * 4;
+                                  (RATE ? 2 : 1) * 32 * PSTRIDE * 4 + 16;  // + segment-run state (MODE 1)
   __host__ __device__ static constexpr size_t bytes() { return BYTES; }
 };
 
@@ -79,8 +147,10 @@ __host__ __device__ inline size_t replay_head_bytes(int D, int B) {
 #define ORLOJ_REPLAY_MIN_BLOCKS 8
 #endif
 
-template <int BPL, bool RATE, bool ALG1 = false>
-__global__ void __launch_bounds__(REPLAY_WARPS * 32, ORLOJ_REPLAY_MIN_BLOCKS)
+// MODE 0: plain replay, one warp per scenario.  MODE 1: speculative segments,
+// one warp per (scenario, segment).  MODE 2: stitch, one warp per scenario.
+template <int BPL, bool RATE, bool ALG1 = false, int MODE = 0>
+__global__ void __launch_bounds__(REPLAY_WARPS * 32, MODE == 2 ? 2 : ORLOJ_REPLAY_MIN_BLOCKS)
 replay_kernel(const __grid_constant__ ReplayParams p) {
   constexpr int STG = ReplayWarpSmem<BPL, RATE>::STG;
   constexpr int PST = ReplayWarpSmem<BPL, RATE>::PSTRIDE;
@@ -100,6 +170,11 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int32_t *w_tb = w_d + 32;                                                 // window true bins
   float *Pm = reinterpret_cast<float *>(w_tb + 32);                         // P[k-1][r], stride PST
   float *Sm = Pm + 32 * PST;  // RATE only: per-lane partial sum_{i<B} G_k(tau_i), [k-1][lane]
+  // MODE 1 (cold, warp-uniform; kept out of registers): base arrival of the
+  // current record list, records in it, extension flag
+  int64_t *sm_mark_base = reinterpret_cast<int64_t *>(Sm + (RATE ? 32 * PST : 0));
+  int32_t *sm_nrec = reinterpret_cast<int32_t *>(sm_mark_base + 1);
+  int32_t *sm_ext = sm_nrec + 1;
 
   // stage the (small) store; hopeless threshold a_1 + w_1 m_min(d) per distribution
   for (int e = threadIdx.x; e < D * B; e += blockDim.x) s_store[e] = p.log2F[e];
@@ -114,8 +189,18 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   if (lane < REPLAY_KB) stg[lane * STG - 1] = -INFINITY;
   __syncthreads();
 
-  const int64_t s = (int64_t)blockIdx.x * REPLAY_WARPS + wid;
-  if (s >= p.S) return;
+  if constexpr (MODE == 1)
+    if (blockIdx.x == 0 && threadIdx.x < 4) p.seg_stats[threadIdx.x] = 0;  // read after this launch only
+  const int64_t u = (int64_t)blockIdx.x * REPLAY_WARPS + wid;
+  int64_t s = u;
+  int g = 0;  // MODE 1: this warp's segment; MODE 2: the segment being stitched
+  if constexpr (MODE == 1) {
+    if (u >= p.S * p.G) return;
+    s = u / p.G;
+    g = (int)(u - s * p.G);
+  } else {
+    if (s >= p.S) return;
+  }
 
   const int kmax = p.prof.kmax;
   const int64_t base = p.arr_off[s];
@@ -137,17 +222,144 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
 
   int64_t t = INT64_MIN;
   int64_t cursor = 0;
+  int64_t seg_end = INT64_MAX;  // MODE 1: stop (s_{g+1}, then the extension cap); MODE 2: s_{g+1} of the stitched g
+  int64_t rec_at = INT64_MAX;  // MODE 1: record the first regeneration point at or past this arrival
+  ReplaySeg *sg = nullptr;               // MODE 1: this segment; MODE 2: the scenario's segments
+  int32_t *mylog = p.log ? p.log + base + s : nullptr;
+  if constexpr (MODE == 1) {
+    cursor = seg_begin(n, g, p.G);
+    if (g > 0) rec_at = cursor;  // segment 0's records are never matched
+    if (lane == 0) {
+      *sm_mark_base = cursor;
+      *sm_nrec = 0;
+      *sm_ext = 0;
+    }
+    __syncwarp();
+    if (g + 1 < p.G) seg_end = seg_begin(n, g + 1, p.G);
+    sg = p.seg + u;
+    if (g > 0) mylog = p.seg_log ? p.seg_log + seg_log_off(base, s, n, g, p.G) : nullptr;
+  }
   // lookahead: lane l holds arrivals[cursor + l] (arrival INT64_MAX beyond the trace)
   int64_t ua = INT64_MAX;
   int ud = 0, ut = 0;
-  if (lane < n) {
-    ua = arr[lane];
-    ud = dis[lane];
-    ut = tbs[lane];
-  }
+  auto reload = [&]() {
+    const int64_t idx = cursor + lane;
+    ua = INT64_MAX;
+    if (idx < n) {
+      ua = arr[idx];
+      ud = dis[idx];
+      ut = tbs[idx];
+    }
+  };
+  reload();
   int ncarry = 0, carry_off = 0;
   long long c_fin = 0, c_drop = 0, c_late = 0, c_bat = 0, c_busy = 0;
   int64_t ndec = 0;
+  int nrec = 0;  // MODE 1: records in the current list; MODE 2: match pointer into segment g's records
+  int64_t taken = 0;  // MODE 2: decisions taken over from segment runs (the rest were re-run here)
+  int joined = 0, crossed = 0;
+
+  // MODE 1: end state of the segment run
+  auto save_end = [&]() {
+    if (lane < ncarry) {
+      sg->carry_D[lane] = w_dl[carry_off + lane];
+      sg->carry_h[lane] = w_h[carry_off + lane];
+      sg->carry_d[lane] = w_d[carry_off + lane];
+      sg->carry_tb[lane] = w_tb[carry_off + lane];
+    }
+    if (lane == 0) {
+      sg->t = t;
+      sg->cursor = cursor;
+      sg->ndec = ndec;
+      sg->ctr[0] = c_fin;
+      sg->ctr[1] = c_drop;
+      sg->ctr[2] = c_late;
+      sg->ctr[3] = c_bat;
+      sg->ctr[4] = c_busy;
+      sg->ncarry = ncarry;
+      sg->nrec = nrec;
+    }
+  };
+  // MODE 2: decision log of segment gg's run (segment 0 wrote the true log)
+  auto seg_src_log = [&](int gg) -> const int32_t * {
+    return gg == 0 ? p.log + base + s : p.seg_log + seg_log_off(base, s, n, gg, p.G);
+  };
+  // MODE 2: append segment gg's decisions [from, to) and its counters between two of its points
+  auto take = [&](int gg, long long from, long long to, const long long *c0, const long long *c1) {
+    if (mylog) {
+      const int32_t *src = seg_src_log(gg);
+      for (long long i = from + lane; i < to; i += 32) mylog[ndec + i - from] = src[i];
+    }
+    c_fin += c1[0] - c0[0];
+    c_drop += c1[1] - c0[1];
+    c_late += c1[2] - c0[2];
+    c_bat += c1[3] - c0[3];
+    c_busy += c1[4] - c0[4];
+    ndec += to - from;
+    taken += to - from;
+  };
+  // MODE 2: load segment gg's end state into the registers / window (the true state)
+  auto materialize = [&](const ReplaySeg *e) {
+    t = e->t;
+    cursor = e->cursor;
+    ncarry = e->ncarry;
+    carry_off = 0;
+    __syncwarp();
+    if (lane < ncarry) {
+      w_dl[lane] = e->carry_D[lane];
+      w_h[lane] = e->carry_h[lane];
+      w_d[lane] = e->carry_d[lane];
+      w_tb[lane] = e->carry_tb[lane];
+    }
+    __syncwarp();
+    reload();
+  };
+  // MODE 2: the true run is at segment g-1's end state (not loaded): while the
+  // extension of segment g-1 and the records of segment g share a regeneration
+  // point, the true run is segment g-1's extension up to it and segment g's run
+  // from it — join without re-running anything.  Returns true once the last
+  // segment is joined (the true run ends at its end state).
+  auto lazy_walk = [&]() -> bool {
+    while (g < p.G) {
+      const ReplaySeg *pe = sg + g - 1, *e = sg + g;
+      const int ne = pe->next, nr = e->nrec;
+      const long long ja = lane < ne ? pe->ext[lane].j : -1;
+      const long long jb = lane < nr ? e->rec[lane].j : -2;
+      int hit = -1;
+      for (int b2 = 0; b2 < nr; ++b2) {
+        const long long x = __shfl_sync(FULL, jb, b2);
+        if (x == ja && hit < 0) hit = b2;
+      }
+      const unsigned hm = __ballot_sync(FULL, hit >= 0);
+      if (hm == 0) return false;
+      const int ia = __ffs(hm) - 1;  // lists increase: the first common point
+      const int ib = __shfl_sync(FULL, hit, ia);
+      take(g - 1, pe->ndec, pe->ext[ia].ndec, pe->ctr, pe->ext[ia].ctr);
+      take(g, e->rec[ib].ndec, e->ndec, e->rec[ib].ctr, e->ctr);
+      ++joined;
+      ++g;
+    }
+    return true;
+  };
+  if constexpr (MODE == 2) {
+    // segment 0 ran from the true start: the true run is at its end state
+    sg = p.seg + s * p.G;
+    ndec = sg[0].ndec;  // segment 0 wrote its decisions into the true log
+    taken = ndec;
+    c_fin = sg[0].ctr[0];
+    c_drop = sg[0].ctr[1];
+    c_late = sg[0].ctr[2];
+    c_bat = sg[0].ctr[3];
+    c_busy = sg[0].ctr[4];
+    g = 1;
+    if (lazy_walk()) {  // joined everything: the true run ends at the last segment's end state
+      t = sg[p.G - 1].t;
+      cursor = n;
+    } else {
+      materialize(sg + g - 1);
+      seg_end = g + 1 < p.G ? seg_begin(n, g + 1, p.G) : INT64_MAX;
+    }
+  }
 
   // consume m (< 32) arrivals from the lookahead: shift by m lanes, refill the
   // tail from HBM (used from the next decision on)
@@ -174,6 +386,70 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int64_t a1 = p.prof.a[0], w1 = p.prof.w[0];
 
   while (cursor < n || ncarry > 0) {
+    if constexpr (MODE == 1) {
+      if (cursor >= seg_end) {  // first loop top past the segment: its end state, then the extension
+        if (*sm_ext) break;
+        nrec = *sm_nrec;
+        save_end();
+        rec_at = seg_end;
+        __syncwarp();
+        if (lane == 0) {
+          *sm_ext = 1;
+          *sm_mark_base = seg_end;
+          *sm_nrec = 0;
+        }
+        __syncwarp();
+        seg_end = seg_begin(n, g + 2, p.G);
+      }
+      if (cursor >= rec_at && ncarry == 0) {
+        const int64_t a0 = __shfl_sync(FULL, ua, 0);
+        if (a0 != INT64_MAX && t <= a0) {  // regeneration point at arrival `cursor`: record it
+          const int nr = *sm_nrec;
+          const bool ext = *sm_ext;
+          const int64_t mb = *sm_mark_base;
+          const long long v = lane == 0 ? cursor : lane == 1 ? ndec : lane == 2 ? c_fin : lane == 3 ? c_drop
+                              : lane == 4 ? c_late : lane == 5 ? c_bat : c_busy;
+          if (lane < 7) reinterpret_cast<long long *>(ext ? &sg->ext[nr] : &sg->rec[nr])[lane] = v;
+          int64_t m = rec_at - mb;
+          while (m <= cursor - mb) m = seg_next_mark(m);
+          rec_at = nr + 1 < SEG_REC ? mb + m : INT64_MAX;
+          __syncwarp();
+          if (lane == 0) *sm_nrec = nr + 1;
+          __syncwarp();
+          if (ext && nr + 1 > SEG_EXT_AFTER) break;
+        }
+      }
+    }
+    if constexpr (MODE == 2) {
+      if (cursor >= seg_end) {  // the true run crossed segment g without meeting it: next segment
+        ++crossed;
+        ++g;
+        nrec = 0;
+        seg_end = g + 1 < p.G ? seg_begin(n, g + 1, p.G) : INT64_MAX;
+        continue;
+      }
+      if (g < p.G && ncarry == 0) {
+        const int64_t a0 = __shfl_sync(FULL, ua, 0);
+        if (a0 != INT64_MAX && t <= a0) {  // true run regenerates at arrival `cursor`
+          const ReplaySeg *e = sg + g;
+          const int nr = e->nrec;
+          while (nrec < nr && e->rec[nrec].j < cursor) ++nrec;
+          if (nrec < nr && e->rec[nrec].j == cursor) {  // segment g regenerated here too: same run from now on
+            take(g, e->rec[nrec].ndec, e->ndec, e->rec[nrec].ctr, e->ctr);
+            ++joined;
+            ++g;
+            nrec = 0;
+            if (lazy_walk()) {
+              t = sg[p.G - 1].t;
+              break;
+            }
+            materialize(sg + g - 1);
+            seg_end = g + 1 < p.G ? seg_begin(n, g + 1, p.G) : INT64_MAX;
+            continue;
+          }
+        }
+      }
+    }
     // ---- 0. runs of single-member windows (max-plus scan) -----------------
     // With nothing carried, arrival j of the lookahead is a window of one iff
     // it is not hopeless at its decision time t'_j = max(T_{j-1}, a_j) and the
@@ -214,7 +490,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         c_bat += m;
         c_busy += __shfl_sync(FULL, P, m - 1);
         t = __shfl_sync(FULL, Tj, m - 1);
-        if (p.log && lane < m) p.log[base + s + ndec + lane] = 1;
+        if (mylog && lane < m) mylog[ndec + lane] = 1;
         ndec += m;
         advance(m);
         continue;
@@ -420,7 +696,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     c_bat += 1;
     c_busy += dur;
     t += dur;
-    if (p.log && lane == 0) p.log[base + s + ndec] = ALG1 ? (int32_t)selm : kstar;
+    if (mylog && lane == 0) mylog[ndec] = ALG1 ? (int32_t)selm : kstar;
     ++ndec;
     ncarry = wc - kstar;
     carry_off = kstar;
@@ -440,8 +716,25 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
     __syncwarp();
   }
+  if constexpr (MODE == 1) {
+    const bool ext = *sm_ext;
+    nrec = *sm_nrec;
+    if (!ext) save_end();  // ended before s_{g+1} (last segment, or the trace ran out)
+    if (lane == 0) {
+      sg->next = ext ? nrec : 0;
+      if (ext) atomicAdd(p.seg_stats + 3, (unsigned long long)(ndec - sg->ndec));
+    }
+    return;
+  }
+  if constexpr (MODE == 2) {
+    if (lane == 0) {
+      atomicAdd(p.seg_stats + 0, (unsigned long long)(ndec - taken));
+      atomicAdd(p.seg_stats + 1, (unsigned long long)joined);
+      atomicAdd(p.seg_stats + 2, (unsigned long long)crossed);
+    }
+  }
   if (lane == 0) {
-    if (p.log) p.log[base + s + ndec] = 0;
+    if (mylog) mylog[ndec] = 0;
     unsigned long long *cs = p.counters + (int64_t)p.bucket[s] * 7;
     atomicAdd(cs + 0, (unsigned long long)n);
     atomicAdd(cs + 1, (unsigned long long)c_fin);

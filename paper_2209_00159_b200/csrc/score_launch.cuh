@@ -1,0 +1,72 @@
+// score_launch.cuh — template dispatch of score_kernel<BPL, SLOTS, PICK,
+// STREAM, SMEMS>; the PICK = true / false halves are instantiated in their own
+// translation units (score_pick.cu, score_all.cu) so the library builds in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+#include "common.cuh"
+#include "host_util.h"
+#include "score_kernel.cuh"
+
+namespace orloj {
+namespace host {
+
+// Row source of the score kernel: TMA ring from HBM (STREAM adds L1 bypass and
+// L2 evict-first for stores larger than L2), or the whole store staged in
+// shared memory when it is small (a few application histograms).
+enum class RowSrc { Tma, TmaStream, Smem };
+constexpr int64_t STREAM_STORE_BYTES = 256ll << 20;
+constexpr int64_t SMEM_STORE_BYTES = 48ll << 10;
+
+template <int BPL, int SLOTS, bool PICK, bool STREAM, bool SMEMS>
+cudaError_t launch_score_t(const ScoreParams &p, cudaStream_t s) {
+  const int64_t blocks = (p.Q + SCORE_WARPS - 1) / SCORE_WARPS;
+  const size_t base = ScoreShape<BPL>::smem_bytes();
+  const size_t smem = base + (SMEMS ? (size_t)p.D * p.B * 4 : 0);
+  const size_t cap = base + (SMEMS ? (size_t)SMEM_STORE_BYTES : 0);
+  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
+  if (!configured.load(std::memory_order_acquire)) {
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_release);
+  }
+  score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS><<<(unsigned)blocks, SCORE_WARPS * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int BPL, bool PICK, bool STREAM, bool SMEMS>
+cudaError_t launch_score_s(const ScoreParams &p, cudaStream_t s) {
+  switch (slots_for(p.kmax)) {
+    case 1: return launch_score_t<BPL, 1, PICK, STREAM, SMEMS>(p, s);
+    case 2: return launch_score_t<BPL, 2, PICK, STREAM, SMEMS>(p, s);
+    case 4: return launch_score_t<BPL, 4, PICK, STREAM, SMEMS>(p, s);
+    default: return launch_score_t<BPL, 8, PICK, STREAM, SMEMS>(p, s);
+  }
+}
+
+template <int BPL, bool PICK>
+cudaError_t launch_score_r(const ScoreParams &p, RowSrc src, cudaStream_t s) {
+  if (src == RowSrc::Smem) return launch_score_s<BPL, PICK, false, true>(p, s);
+  if constexpr (BPL == 8)
+    if (src == RowSrc::TmaStream) return launch_score_s<8, PICK, true, false>(p, s);
+  return launch_score_s<BPL, PICK, false, false>(p, s);
+}
+
+template <bool PICK>
+inline cudaError_t launch_score_b(const ScoreParams &p, RowSrc src, cudaStream_t s) {
+  switch (bins_per_lane(p.B)) {
+    case 1: return launch_score_r<1, PICK>(p, src, s);
+    case 2: return launch_score_r<2, PICK>(p, src, s);
+    case 4: return launch_score_r<4, PICK>(p, src, s);
+    default: return launch_score_r<8, PICK>(p, src, s);
+  }
+}
+
+cudaError_t launch_score_pick(const ScoreParams &p, RowSrc src, cudaStream_t s);
+cudaError_t launch_score_all(const ScoreParams &p, RowSrc src, cudaStream_t s);
+
+}  // namespace host
+}  // namespace orloj

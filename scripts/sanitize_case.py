@@ -33,6 +33,9 @@ def main():
     f.trace.validate(f.store)
     orj.replay_trace(f.store, f.profile, f.trace, decision_log=True)
     orj.replay_trace(f.store, f.profile, f.trace, objective="finish_rate")
+    # segmented replay (speculative segments + stitch), with and without the log
+    orj.replay_trace(f.store, f.profile, f.trace, decision_log=True, segments=5)
+    orj.replay_trace(f.store, f.profile, f.trace, segments=3, objective="finish_rate")
     # Alg. 1 policy (priority tables inside the replay kernel)
     from paper_2209_00159_b200 import policy
     pt = orj.PriorityTable(f.store, f.profile, f.profile.kmax, 1.0 / f.tf.fam.mean_ticks())

@@ -1,0 +1,130 @@
+"""GPU parity of the segmented replay (orloj_replay_trace_seg, include/orloj.h):
+speculative segments stitched at regeneration points must give the plain
+replay's counters and decision log bit for bit, for every policy, segment
+count and the degenerate traces (empty / one-arrival scenarios, bursts with no
+regeneration point, more segments than arrivals); and the oracle, following
+the segmented log, reproduces the counters."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2209_00159_b200 as orj  # noqa: E402
+import workloads as wl  # noqa: E402
+from paper_2209_00159_b200 import policy  # noqa: E402
+
+
+def _family(fam, seeds, n):
+    tf = gen.c5_trace_family(fam)
+    gids, bucket, slo = gen.c5_scenarios(tf, seeds)
+    arr, dist, tb = gen.trace_host(tf, gids, n)
+    off = np.arange(len(gids) + 1, dtype=np.int64) * n
+    return tf, off, arr, dist, tb, slo
+
+
+def _trace(off, arr, dist, tb, slo):
+    S = len(slo)
+    return orj.Trace(wl.t(off, np.int64), wl.t(arr, np.int64), wl.t(dist, np.int32), wl.t(tb, np.int16),
+                     wl.t(slo, np.int64), wl.t(np.arange(S), np.int32), S)
+
+
+def _kw(tf, store, prof, objective, drop):
+    kw = dict(objective=objective)
+    if drop == "expected_latency":
+        kw["drop_threshold"] = wl.t(policy.expected_latency_thresholds(tf.fam.counts, tf.profile.a, tf.profile.w),
+                                    np.int64)
+    if objective == "alg1":
+        a, w = tf.profile.a, tf.profile.w
+        kw["priority"] = orj.PriorityTable(store, prof, len(a), 1.0 / float(np.mean(a + w * 8)))
+        kw["size_thresholds"] = wl.t(policy.alg1_size_thresholds(tf.fam.counts, a, w), np.int64)
+    return kw
+
+
+def _both(store, prof, tr, segments, **kw):
+    pb0, log0 = orj.replay_trace(store, prof, tr, decision_log=True, **kw)
+    pb1, log1 = orj.replay_trace(store, prof, tr, decision_log=True, segments=segments, **kw)
+    pb2, _ = orj.replay_trace(store, prof, tr, segments=segments, **kw)  # without a log
+    torch.cuda.synchronize()
+    return pb0.cpu().numpy(), log0.cpu().numpy(), pb1.cpu().numpy(), log1.cpu().numpy(), pb2.cpu().numpy()
+
+
+@pytest.mark.parametrize("fam", gen.C5_FAMILIES)
+@pytest.mark.parametrize("objective,drop", [("expected_finish", "hopeless"), ("finish_rate", "expected_latency"),
+                                            ("alg1", "hopeless")])
+def test_segmented_equals_plain(fam, objective, drop):
+    """32 scenarios (all 8 SLO buckets) x 20,000 arrivals; 2, 7 and 64 segments."""
+    tf, off, arr, dist, tb, slo = _family(fam, 4, 20000)
+    store = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks)
+    prof = orj.LatencyProfile(tf.profile.a, tf.profile.w)
+    tr = _trace(off, arr, dist, tb, slo)
+    kw = _kw(tf, store, prof, objective, drop)
+    for G in (2, 7, 64):
+        pb0, log0, pb1, log1, pb2 = _both(store, prof, tr, G, **kw)
+        assert (pb1 == pb0).all(), (G, np.argwhere(pb1 != pb0)[:5])
+        assert (pb2 == pb0).all(), G
+        assert (log1 == log0).all(), (G, np.flatnonzero(log1 != log0)[:5])
+
+
+def test_segmented_follow_oracle():
+    """The oracle follows the segmented replay's log: decisions in its tie sets,
+    counters bit-exact."""
+    tf, off, arr, dist, tb, slo = _family("skipnet", 8, 20000)
+    store = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks)
+    prof = orj.LatencyProfile(tf.profile.a, tf.profile.w)
+    pb, log = orj.replay_trace(store, prof, _trace(off, arr, dist, tb, slo), decision_log=True, segments=16)
+    torch.cuda.synchronize()
+    pb, log = pb.cpu().numpy(), log.cpu().numpy()
+    ref = oracle.replay(oracle.cdf(tf.fam.counts), tf.profile.a, tf.profile.w, off, arr, dist, tb, slo,
+                        follow_log=log)
+    assert (ref["ties"][:, 2] == -1).all()
+    assert (pb == ref["counters"]).all()
+    assert (pb[:, 1] + pb[:, 2] + pb[:, 3] == pb[:, 0]).all()
+
+
+def test_segmented_edges():
+    """Empty and one-arrival scenarios, a simultaneous burst (no regeneration
+    point until it drains: the stitch runs through every segment), a trace of
+    back-to-back overload, and more segments than arrivals."""
+    tf = gen.c5_trace_family("gpt")
+    gids, bucket, slo = gen.c5_scenarios(tf, 2)
+    S = len(gids)
+    n = 3000
+    arr, dist, tb = gen.trace_host(tf, gids, n)
+    arr = arr.reshape(S, n)
+    arr[1, :] = arr[1, 0]                                     # one huge simultaneous burst
+    arr[3, :] = arr[3, 0] + np.arange(n) * 10                 # arrivals far faster than service
+    lens = np.full(S, n)
+    lens[0], lens[2], lens[5] = 0, 1, 33
+    keep = np.concatenate([np.arange(s * n, s * n + lens[s]) for s in range(S)])
+    arr, dist, tb = arr.reshape(-1)[keep], dist[keep], tb[keep]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    store = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks)
+    prof = orj.LatencyProfile(tf.profile.a, tf.profile.w)
+    tr = _trace(off, arr, dist, tb, slo)
+    for G in (2, 3, 31, 4096):
+        pb0, log0, pb1, log1, pb2 = _both(store, prof, tr, G)
+        assert (pb1 == pb0).all() and (pb2 == pb0).all() and (log1 == log0).all(), G
+    assert pb0[0].tolist() == [0] * 7 and pb0[2, 0] == 1
+
+
+def test_segmented_arguments():
+    tf, off, arr, dist, tb, slo = _family("static", 1, 100)
+    store = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks)
+    prof = orj.LatencyProfile(tf.profile.a, tf.profile.w)
+    tr = _trace(off, arr, dist, tb, slo)
+    need = orj.replay_seg_workspace_bytes(tr, 4)
+    assert need > 0 and orj.replay_seg_workspace_bytes(tr, 1) == 0
+    assert orj.replay_seg_workspace_bytes(tr, 4, True) > need
+    small = torch.empty(need - 256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(orj.OrlojError, match="workspace"):
+        orj.replay_trace(store, prof, tr, segments=4, workspace=small)
+    with pytest.raises(orj.OrlojError, match="segments"):
+        orj.replay_trace(store, prof, tr, segments=0)
+    with pytest.raises(orj.OrlojError, match="segments"):
+        orj.replay_trace(store, prof, tr, segments=5000)
