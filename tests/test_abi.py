@@ -61,3 +61,28 @@ def test_cubin_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", _abi.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_replay_seg_workspace(lib):
+    """Workspace of the segmented replay: none for 1 segment; 256 B of stats +
+    the per-segment states, + 4 (2N + 34 S G) bytes of scratch log with a log."""
+    f = lib.orloj_replay_seg_workspace
+    assert f(8, 1000, 1, 0) == 0 and f(0, 0, 4, 0) == 0
+    base = f(8, 1000, 4, 0)
+    assert base > 256 and base % 256 == 0
+    assert f(8, 1000, 8, 0) > base
+    with_log = f(8, 1000, 4, 1)
+    assert with_log - base >= 4 * (2 * 1000 + 34 * 8 * 4)
+    st = _abi.Store(1, 8, 1, 16)
+    a = np.zeros(1, np.int64)
+    w = np.ones(1, np.int64)
+    prof = _abi.LatencyProfile(1, a.ctypes.data, w.ctypes.data)
+    tr = _abi.TraceC(2, 16, 16, 16, 16, 16, 16, 1)
+    pol = _abi.ReplayPolicyC(0, None, None, None, None, 0.0)
+    p = ctypes.c_void_p(16)
+    assert lib.orloj_replay_trace_seg(ctypes.byref(st), ctypes.byref(prof), ctypes.byref(tr), ctypes.byref(pol), 0,
+                                      10, p, 0, p, None, None) == 1
+    assert b"segments" in lib.orloj_last_error()
+    assert lib.orloj_replay_trace_seg(ctypes.byref(st), ctypes.byref(prof), ctypes.byref(tr), ctypes.byref(pol), 4,
+                                      10, None, 0, p, None, None) == 1
+    assert b"workspace" in lib.orloj_last_error()
