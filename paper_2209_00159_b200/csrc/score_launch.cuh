@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "host_util.h"
 #include "score_kernel.cuh"
+#include "score_small_kernel.cuh"
 
 namespace orloj {
 namespace host {
@@ -55,8 +56,27 @@ cudaError_t launch_score_r(const ScoreParams &p, RowSrc src, cudaStream_t s) {
   return launch_score_s<BPL, PICK, false, false>(p, s);
 }
 
+// short queues over a small store: lanes over candidate sizes (score_small_kernel.cuh)
+template <int BPL, bool PICK>
+cudaError_t launch_score_small(const ScoreParams &p, cudaStream_t s) {
+  const int64_t blocks = (p.Q + SMALL_WARPS - 1) / SMALL_WARPS;
+  const size_t smem = SmallShape<BPL>::bytes(p.D, p.B);
+  static std::atomic<bool> configured{false};
+  if (!configured.load(std::memory_order_acquire)) {
+    const size_t cap = SmallShape<BPL>::bytes((int)(SMEM_STORE_BYTES / (32 * BPL * 4)), 32 * BPL);
+    cudaError_t e = cudaFuncSetAttribute(score_small_kernel<BPL, PICK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)cap);
+    if (e != cudaSuccess) return e;
+    configured.store(true, std::memory_order_release);
+  }
+  score_small_kernel<BPL, PICK><<<(unsigned)blocks, SMALL_WARPS * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <bool PICK>
 inline cudaError_t launch_score_b(const ScoreParams &p, RowSrc src, cudaStream_t s) {
+  if (src == RowSrc::Smem && p.kmax <= 32 && p.B <= 64 && !p.P && !p.EL)
+    return p.B <= 32 ? launch_score_small<1, PICK>(p, s) : launch_score_small<2, PICK>(p, s);
   switch (bins_per_lane(p.B)) {
     case 1: return launch_score_r<1, PICK>(p, src, s);
     case 2: return launch_score_r<2, PICK>(p, src, s);

@@ -1,0 +1,113 @@
+// score_small_kernel.cuh — K1/K2 for short queues over a small store (kmax <= 32,
+// B <= 64, the store staged in shared memory: C1, C2, C4 of SURVEY §8(d)).
+//
+// Same quantities as score_kernel.cuh, laid out for
+// queues that fit one warp:
+//   LG_k[i] = LG_{k-1}[i] + log2 F_{d_k}(tau_i)   lanes over bins; rows LG_1..LG_K
+//                                                   staged in shared memory, each
+//                                                   with a -inf head for i* = 0
+//   lane k-1 then owns candidate size k: its lookup constants (a_k, w_k) sit in
+//   registers, it walks the members r = 1..k (sigma_r broadcast by shuffle) and
+//   sums  E_k = sum_{r<=k} 2^{LG_k[i*(r,k)]}  itself — no reduction tree.
+// The adds that build LG_k are the same fp32 adds in the same order as
+// score_kernel's, so LG and every P_r(k) are identical; E_k is a sequential
+// fp32 sum over r (score_kernel: a tree), within the same 1e-5 k tolerance.
+// Argmax: two REDUX (max of float bits, then min k).  Used by pick and by
+// score when neither P nor E[L_B] is requested.
+#pragma once
+#include "common.cuh"
+#include "score_kernel.cuh"
+
+namespace orloj {
+
+constexpr int SMALL_WARPS = 8;
+
+// shared memory: store [D][B] | profile int4 [32] | per warp LG rows [32][32 BPL + 1]
+template <int BPL>
+struct SmallShape {
+  static constexpr int ROW = 32 * BPL + 1;  // odd row stride: rows start on different banks
+  __host__ __device__ static size_t bytes(int D, int B) {
+    return (((size_t)D * B * 4 + 15) & ~(size_t)15) + 32 * 16 + (size_t)SMALL_WARPS * 32 * ROW * 4;
+  }
+};
+
+template <int BPL, bool PICK>
+__global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __grid_constant__ ScoreParams p) {
+  constexpr int ROW = SmallShape<BPL>::ROW;
+  extern __shared__ __align__(16) float s_dyn[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int D = p.D, B = p.B, kmax = p.kmax;
+  float *s_store = s_dyn;
+  int4 *s_prof = reinterpret_cast<int4 *>(s_dyn + (((size_t)D * B + 3) & ~(size_t)3));
+  float *lgs = reinterpret_cast<float *>(s_prof + 32) + wid * 32 * ROW;  // row k-1 = LG_k; [0] = -inf
+
+  for (int e = threadIdx.x * 4; e < D * B; e += blockDim.x * 4)
+    *reinterpret_cast<float4 *>(s_store + e) = __ldg(reinterpret_cast<const float4 *>(p.log2F + e));
+  if (threadIdx.x < kmax)
+    s_prof[threadIdx.x] = make_int4(p.prof.a2[threadIdx.x], p.prof.wB2[threadIdx.x], (int)p.prof.mag[threadIdx.x],
+                                    (int)p.prof.sh[threadIdx.x]);
+  lgs[lane * ROW] = -INFINITY;
+  __syncthreads();
+
+  const int64_t q = (int64_t)blockIdx.x * SMALL_WARPS + wid;
+  if (q >= p.Q) return;
+  const int64_t off = p.offsets[q] - p.offsets[0];  // offsets may start at any base (chunked calls)
+  const int64_t n = p.offsets[q + 1] - p.offsets[q];
+  const int K = (int)(n < kmax ? n : kmax);
+  const int64_t now = p.now[q];
+  const int32_t sig = lane < K ? sigma2(p.deadline[off + lane] - now) : 0;
+  const int id = lane < K ? p.dist[off + lane] : 0;
+  const int4 pk = s_prof[lane < kmax ? lane : 0];
+
+  // a2: LG_k for k = 1..K, lanes over bins (bin lane + 32 e + 1)
+  float acc[BPL];
+#pragma unroll
+  for (int e = 0; e < BPL; ++e) acc[e] = 0.f;
+  for (int k = 0; k < K; ++k) {
+    const float *src = s_store + __shfl_sync(FULL, id, k) * B;
+#pragma unroll
+    for (int e = 0; e < BPL; ++e) {
+      const int bin = lane + 32 * e;
+      if (bin < B) {
+        acc[e] += src[bin];
+        lgs[k * ROW + 1 + bin] = acc[e];
+      }
+    }
+  }
+  __syncwarp();
+
+  // a3-a5: lane k-1 sums P_r(k) over its members r = 1..k
+  const float *row = lgs + lane * ROW;
+  float E = 0.f;
+  int r = 0;
+  for (; r + 4 <= K; r += 4) {
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      v[j] = ex2_approx(row[lookup_bin(__shfl_sync(FULL, sig, r + j), pk.x, pk.y, (uint32_t)pk.z, (uint32_t)pk.w)]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) E += r + j <= lane ? v[j] : 0.f;
+  }
+  for (; r < K; ++r) {
+    const float v = ex2_approx(row[lookup_bin(__shfl_sync(FULL, sig, r), pk.x, pk.y, (uint32_t)pk.z, (uint32_t)pk.w)]);
+    E += r <= lane ? v : 0.f;
+  }
+
+  // a6: argmax, ties -> smallest k (E >= 0: float bits order like values)
+  const int k = lane + 1;
+  const bool valid = k <= K;
+  if constexpr (PICK) {
+    const uint32_t bits = valid ? __float_as_uint(E) : 0u;
+    const uint32_t mx = __reduce_max_sync(FULL, bits);
+    const uint32_t kb = __reduce_min_sync(FULL, (valid && bits == mx) ? (uint32_t)k : 0x7fffffffu);
+    if (lane == 0) {
+      p.best_k[q] = K == 0 ? 0 : (int32_t)kb;
+      p.best_E[q] = K == 0 ? 0.f : __uint_as_float(mx);
+    }
+  } else {
+    if (k <= kmax && p.E) p.E[q * kmax + k - 1] = valid ? E : 0.f;
+  }
+}
+
+}  // namespace orloj
