@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--no-policies", action="store_true", help="skip the replay policy-variant sweep")
     ap.add_argument("--policy-seeds", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--e2e-chunks", type=int, default=32)
+    ap.add_argument("--e2e-streams", type=int, default=3)
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 workload lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -390,7 +391,7 @@ def main():
         pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()  # noqa: E731
         h_off, h_dl = pin(qn.offsets, np.int64), pin(qn.deadline, np.int64)
         h_dist, h_now = pin(qn.dist, np.int32), pin(qn.now, np.int64)
-        hp = orj.HostPicker(store, prof, qn.offsets, chunks=args.e2e_chunks, streams=2, device=dev)
+        hp = orj.HostPicker(store, prof, qn.offsets, chunks=args.e2e_chunks, streams=args.e2e_streams, device=dev)
         for _ in range(max(1, args.warmup)):
             hp.pick(h_off, h_dl, h_dist, h_now, stream)
         torch.cuda.synchronize()
@@ -409,7 +410,7 @@ def main():
                          "h2d_bytes_per_step": hp.h2d_bytes(), "d2h_bytes_per_step": hp.d2h_bytes(),
                          "ms_per_step": e_ms, "steps": e_steps,
                          "path": f"orloj_pick_batch_host: pinned host queues -> H2D -> kernel -> D2H, "
-                                 f"{args.e2e_chunks} chunks pipelined on 2 streams"}
+                                 f"{args.e2e_chunks} chunks pipelined on {args.e2e_streams} streams"}
         del hp
 
     # ---------------- cpu baseline (rank 0, N = 1 only) ----------------
