@@ -83,8 +83,8 @@ static __global__ void priority_table_kernel(const float *__restrict__ log2F, in
 //   sH[k][i] = H[i] - log E[L]   (fp32)
 // Per element (member r, size k), with A = sC[i*] - b sigma (fp64 -> fp32):
 //   no partial bin:  log p = A
-//   partial bin, x = sigma - l1 in (0, w):  g = 1 - e^{-b x} (expm1f),
-//      M = max(A, sH[i*+1]),  log p = M + log(e^{A-M} + e^{sH-M} g)
+//   partial bin, x = sigma - l1 in (0, w):  g = 1 - e^{-b x},
+//      log p = log(e^A + e^{sH[i*+1]} g)  (prio_partial)
 // Output [S][N] (size-major: each store of a warp is one contiguous 128-B
 // line, and PopBatch reads one size row coalesced).
 struct PrioSmem {
@@ -93,6 +93,34 @@ struct PrioSmem {
     return (size_t)S * (16 + 4) + (smem_table ? table_bytes(S, B) : 0);
   }
 };
+
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// The partial bin of Eq. 2 in the log domain: log(e^lp + e^Hn g), g = 1 - e^{-t},
+// t = b x > 0.  g: the Taylor series to t^8 below t = 1/2 (truncation < 2^-26
+// relative, no cancellation), else 1 - 2^{-t log2 e} (g > 0.39 there).  With
+// d = -|lp - Hn| one term of the sum is exactly 1:
+//   lp >= Hn:  lp + log(1 + e^d g),   else  Hn + log(e^d + g),
+// two MUFU (ex2, lg2) per element.
+__device__ __forceinline__ float prio_partial(float lp, float Hn, float t) {
+  float c = -1.f / 40320.f;
+  c = fmaf(c, t, 1.f / 5040.f);
+  c = fmaf(c, t, -1.f / 720.f);
+  c = fmaf(c, t, 1.f / 120.f);
+  c = fmaf(c, t, -1.f / 24.f);
+  c = fmaf(c, t, 1.f / 6.f);
+  c = fmaf(c, t, -0.5f);
+  c = fmaf(c, t, 1.f);
+  const float g = t < 0.5f ? c * t : 1.f - ex2_approx(-t * 1.4426950408889634f);
+  const bool hi = lp >= Hn;
+  const float e = ex2_approx(-fabsf(lp - Hn) * 1.4426950408889634f);
+  const float y = hi ? fmaf(e, g, 1.f) : e + g;
+  return fmaf(0.6931471805599453f, lg2_approx(y), hi ? lp : Hn);
+}
 
 // One element of the score kernel with the table read from global memory
 // (tab_k = table + (k-1) 2 (B+1)); the same arithmetic, value for value, as the
@@ -104,11 +132,7 @@ __device__ __forceinline__ float prio_elem_global(const double *__restrict__ tab
   const double Ci = tab_k[i] - lEL;
   const float Hn = (i < B && x > 0) ? (float)(tab_k[B + 1 + i + 1] - lEL) : -INFINITY;
   float lp = (float)(Ci + bsig);
-  if (Hn > -INFINITY) {
-    const float g = -expm1f(-bf * (float)x);
-    const float M = fmaxf(lp, Hn);
-    lp = M + logf(__expf(lp - M) + __expf(Hn - M) * g);
-  }
+  if (Hn > -INFINITY) lp = prio_partial(lp, Hn, bf * (float)x);
   return lp;
 }
 
@@ -174,11 +198,7 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
       if (part) Hn = (float)(table[(size_t)k * 2 * (B + 1) + B + 1 + i + 1] - lEL);
     }
     float lp = (float)(Ci + bsig);
-    if (Hn > -INFINITY) {
-      const float g = -expm1f(-bf * (float)x);  // 1 - e^{-b x}, 0 < b x < b w
-      const float M = fmaxf(lp, Hn);
-      lp = M + logf(__expf(lp - M) + __expf(Hn - M) * g);
-    }
+    if (Hn > -INFINITY) lp = prio_partial(lp, Hn, bf * (float)x);  // 0 < b x < b w
     return lp;
   };
 
@@ -186,6 +206,9 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
     const int64_t b0 = offsets[q] - base0, e0 = offsets[q + 1] - base0;
     const int64_t t = now[q];
     for (int64_t c0 = b0; c0 < e0; c0 += 32 * PRIO_CHUNK) {
+      // members of this lane in the chunk: c0 + lane + 32 m < e0  <=>  m < nv (32-bit compares below)
+      const int64_t rem = e0 - c0 - lane;
+      const int nv = rem <= 0 ? 0 : rem >= 32 * PRIO_CHUNK ? PRIO_CHUNK : (int)((rem + 31) >> 5);
       double bsig[PRIO_CHUNK];  // -b sigma
       int64_t sg[PRIO_CHUNK];   // sigma (STEPS)
       int32_t s2[PRIO_CHUNK];
@@ -200,12 +223,11 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
       for (int k = 0; k < S; ++k) {
         const int4 lk = s_lk[k];
         const int32_t w = s_w[k];
-        float *ok = out + (int64_t)k * N;
+        float *ok = out + (int64_t)k * N + c0 + lane;  // member m at ok[32 m]
         const double lEL = SMEM_TABLE ? 0.0 : logEL[k];
 #pragma unroll
         for (int m = 0; m < PRIO_CHUNK; ++m) {
-          const int64_t j = c0 + lane + 32 * m;
-          if (j >= e0) break;
+          if (m >= nv) break;
           float lp;
           if (STEPS) {
             lp = -INFINITY;
@@ -215,7 +237,7 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
           } else {
             lp = single(k, lk, w, lEL, s2[m], bsig[m]);
           }
-          ok[j] = lp;
+          ok[32 * m] = lp;
         }
       }
     }
