@@ -57,21 +57,26 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   const int K = (int)(n < kmax ? n : kmax);
   const int64_t now = p.now[q];
   const int32_t sig = lane < K ? sigma2(p.deadline[off + lane] - now) : 0;
-  const int id = lane < K ? p.dist[off + lane] : 0;
+  const int idB = lane < K ? p.dist[off + lane] * B : 0;  // row offset of member lane's distribution
   const int4 pk = s_prof[lane < kmax ? lane : 0];
 
   // a2: LG_k for k = 1..K, lanes over bins (bin lane + 32 e + 1)
   float acc[BPL];
 #pragma unroll
   for (int e = 0; e < BPL; ++e) acc[e] = 0.f;
+  bool bok[BPL];
+#pragma unroll
+  for (int e = 0; e < BPL; ++e) bok[e] = lane + 32 * e < B;
+  const float *s_lane = s_store + lane;
+  float *dst = lgs + 1 + lane;
+#pragma unroll 4
   for (int k = 0; k < K; ++k) {
-    const float *src = s_store + __shfl_sync(FULL, id, k) * B;
+    const float *src = s_lane + __shfl_sync(FULL, idB, k);
 #pragma unroll
     for (int e = 0; e < BPL; ++e) {
-      const int bin = lane + 32 * e;
-      if (bin < B) {
-        acc[e] += src[bin];
-        lgs[k * ROW + 1 + bin] = acc[e];
+      if (bok[e]) {
+        acc[e] += src[32 * e];
+        dst[k * ROW + 32 * e] = acc[e];
       }
     }
   }
