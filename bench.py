@@ -495,9 +495,78 @@ def run_other_workloads(args, dev, max_over_ranks, world):
             out[name]["agreement_with_planner"] = float((bk.cpu().numpy() == planner_k).mean())
         del store, qs
     torch.cuda.empty_cache()
+    out["C1_latency"] = run_c1_latency(dev)
     out["P1"] = run_priority(dev, max_over_ranks, world)
     out["C2_model_variants"] = run_model_variants(dev, max_over_ranks, world)
     return out
+
+
+def run_c1_latency(dev):
+    """Single-decision latency on C1 (1 queue x 8 requests, 16 bins): the
+    pick kernel inside a CUDA graph of 100 launches, and the host round trip a
+    serving scheduler would see (orloj_pick_batch_host: H2D of the queue,
+    kernel, D2H of k*, stream synchronise), timed by the host clock over 2,000
+    calls.  Context only: the paper times its CPU priority queue, not this
+    (< 0.5 ms per insertion)."""
+    import time
+
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+
+    cfg = gen.config1()
+    store = wl.score_store(cfg, dev)
+    prof = wl.profile(cfg.profile)
+    qs = wl.device_queues(cfg.queues, dev, with_arrival=False)
+    bk = torch.empty(1, dtype=torch.int32, device=dev)
+    bE = torch.empty(1, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            orj.pick_batch(store, prof, qs, bk, bE, stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(100):
+            orj.pick_batch(store, prof, qs, bk, bE, stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    graph_us = e0.elapsed_time(e1) * 1e3 / 1000
+    q = cfg.queues
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    h_off, h_dl, h_dist, h_now = pin(q.offsets), pin(q.deadline), pin(q.dist), pin(q.now)
+    from paper_2209_00159_b200 import _abi
+    L = _abi.lib()
+    need = L.orloj_pick_batch_host_workspace(1, int(q.offsets[-1]))
+    wsb = torch.empty(need + 256, dtype=torch.uint8, device=dev)
+    ws = (wsb.data_ptr() + 255) & ~255
+    h_bk = torch.empty(1, dtype=torch.int32).pin_memory()
+    h_bE = torch.empty(1, dtype=torch.float32).pin_memory()
+    args = (store.c(), prof.c(), 1, h_off.data_ptr(), h_dl.data_ptr(), h_dist.data_ptr(), h_now.data_ptr(),
+            h_bk.data_ptr(), h_bE.data_ptr(), ws, need, stream.cuda_stream)
+    call = L.orloj_pick_batch_host
+    for _ in range(20):
+        _abi.check(call(*args))
+        stream.synchronize()
+    n = 2000
+    t0 = time.perf_counter()
+    for _ in range(n):
+        call(*args)
+        stream.synchronize()
+    host_us = (time.perf_counter() - t0) / n * 1e6
+    assert int(h_bk[0]) == int(bk.cpu()[0])
+    return {"workload": "C1: 1 queue x 8 requests, 16 bins, kmax 8", "us_per_pick_in_graph": graph_us,
+            "us_host_round_trip": host_us,
+            "timing": "graph: 10 x CUDA graph of 100 picks (CUDA events); host: 2,000 x (orloj_pick_batch_host "
+                      "called through ctypes + stream synchronise), host clock"}
 
 
 def run_model_variants(dev, max_over_ranks, world):

@@ -167,7 +167,12 @@ orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_prof
  * copies.  queue_offsets_host follows the orloj_queues convention (any base),
  * so a caller can pipeline chunks of one queue set on several streams, each
  * with its own workspace, to overlap copies with compute.  workspace: device, >= orloj_pick_batch_host_workspace(Q, N) bytes,
- * 256-byte aligned. */
+ * 256-byte aligned.  Small calls ((Q+1)*8 + 12 N + 8 Q <= 64 KiB, e.g. one
+ * scheduling decision) whose six host arrays are all pinned and mapped into the
+ * device address space (cudaHostAlloc / registered memory under UVA) take a
+ * zero-copy path: the kernel reads the queues and writes the results in host
+ * memory over PCIe (one launch, no copies; workspace unused and may be NULL);
+ * the results are valid once the stream is synchronised. */
 size_t orloj_pick_batch_host_workspace(int64_t num_queues, int64_t num_members);
 orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency_profile *profile,
                                    int64_t num_queues, const int64_t *queue_offsets_host,

@@ -288,6 +288,8 @@ orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_prof
   return ok();
 }
 
+constexpr int64_t ZERO_COPY_BYTES = 64 << 10;  // host arrays read in place below this size
+
 size_t orloj_pick_batch_host_workspace(int64_t Q, int64_t N) {
   if (Q < 0 || N < 0) return 0;
   return align256((Q + 1) * 8) + align256(N * 8) + align256(N * 4) + align256(Q * 8) + align256(Q * 4) +
@@ -303,6 +305,28 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
   const int64_t N = off_h[Q] - off_h[0];
   if (N < 0 || (N > 0 && (!dl_h || !dist_h)))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: bad member arrays");
+  // Small calls (a scheduler's per-decision call): when every host array is
+  // pinned and mapped into the device address space (UVA), the kernel reads the
+  // queues and writes k* / E* over PCIe directly — one launch, no copies.
+  if ((Q + 1) * 8 + N * 12 + Q * 8 <= ZERO_COPY_BYTES) {
+    const void *hp[6] = {off_h, dl_h, dist_h, now_h, bk_h, bE_h};
+    void *dp[6];
+    bool mapped = true;
+    for (int i = 0; i < 6 && mapped; ++i) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, hp[i]) != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+        mapped = false;
+        cudaGetLastError();
+      } else {
+        dp[i] = at.devicePointer;
+      }
+    }
+    if (mapped) {
+      orloj_queues q{Q, (const int64_t *)dp[0], nullptr, (const int64_t *)dp[1], (const int32_t *)dp[2],
+                     (const int64_t *)dp[3]};
+      return orloj_pick_batch(store, profile, &q, (int32_t *)dp[4], (float *)dp[5], stream);
+    }
+  }
   if (!ws || ((uintptr_t)ws & 255u) || ws_bytes < orloj_pick_batch_host_workspace(Q, N))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: workspace too small or misaligned");
   char *w = (char *)ws;

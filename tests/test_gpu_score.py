@@ -299,9 +299,12 @@ def test_empty_and_host_path():
     bk, bE = orj.pick_batch(store, p, wl.device_queues(q))
     pin = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).pin_memory()  # noqa: E731
     hargs = (pin(q.offsets, np.int64), pin(q.deadline, np.int64), pin(q.dist, np.int32), pin(q.now, np.int64))
-    for chunks, streams in ((1, 1), (5, 2), (300, 3)):
+    pageable = tuple(torch.from_numpy(np.ascontiguousarray(a.numpy())) for a in hargs)
+    # (1, 1): 230 KB per call -> copies; (5, 2) and (300, 3): <= 64 KiB per call
+    # -> zero-copy (mapped pinned memory), or copies for pageable host arrays
+    for chunks, streams, args in ((1, 1, hargs), (5, 2, hargs), (300, 3, hargs), (300, 3, pageable)):
         hp = orj.HostPicker(store, p, q.offsets, chunks=chunks, streams=streams)
-        hk, hE = hp.pick(*hargs)
+        hk, hE = hp.pick(*args)
         torch.cuda.synchronize()
         assert (hk.numpy() == bk.cpu().numpy()).all() and (hE.numpy() == bE.cpu().numpy()).all()
     # queue offsets may start at any base (a chunk of a larger queue set)
