@@ -689,12 +689,12 @@ def build_replay(args, rank, world, dev):
 
 def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
     """Segments per scenario for the segmented replay.  "auto": 8 per scenario
-    while a family has >= 1,024 scenarios on this rank, else 16 (the C5 sweep's
-    measured optimum at 1/2/4/8-GPU shard sizes), never below
-    ~2,000 arrivals per segment."""
+    while a family has >= 1,024 scenarios on this rank, 16 from 512, else 24
+    (the C5 sweep's measured optimum at 1/2/4/8-GPU shard sizes),
+    never below ~2,000 arrivals per segment."""
     if spec != "auto":
         return max(1, int(spec))
-    g = 8 if n_scen_family >= 1024 else 16
+    g = 8 if n_scen_family >= 1024 else 16 if n_scen_family >= 512 else 24
     return int(max(1, min(g, n_arr // 2000, 4096)))
 
 
