@@ -266,9 +266,17 @@ def main():
     import workloads as wl
 
     rank, world, local = dist_env()
+    # ORLOJ_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo collectives -- a
+    # functional check of the N > 1 path on a one-GPU box (its timings mean nothing)
+    shared = os.environ.get("ORLOJ_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     def barrier():
