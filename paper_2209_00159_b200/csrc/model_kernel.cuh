@@ -41,7 +41,7 @@ struct ModelParams {
 
 __host__ __device__ inline size_t model_smem_bytes(int kmax, int B, int D, bool smem_store) {
   return (size_t)kmax * (B + 1) * 8 + (smem_store ? (size_t)D * B * 4 : 0) +
-         (size_t)MODEL_WARPS * ((B + 4) * 4 + 32 * 4);
+         (size_t)MODEL_WARPS * ((B + 4) * 4 + 32 * 4 + 32 * 33 * 4);
 }
 
 template <bool INTERP>
@@ -57,8 +57,9 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __g
   __syncthreads();
   const float *store = p.smem_store ? s_store : p.log2F;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  float *stg = s_warp + wid * ((B + 4) + 32) + 4;  // LG_k row, stg[-1] unused
+  float *stg = s_warp + wid * ((B + 4) + 32 + 32 * 33) + 4;  // LG_k row, stg[-1] unused
   int32_t *s_d = reinterpret_cast<int32_t *>(stg + B);  // member distributions [32]
+  float *part = reinterpret_cast<float *>(s_d + 32);      // [k-1][lane] partial sums, stride 33
   const int64_t q = (int64_t)blockIdx.x * MODEL_WARPS + wid;
   if (q >= p.Q) return;
   const int64_t base0 = p.offsets[0];
@@ -73,8 +74,6 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __g
   float lg[MODEL_MAX_BINS / 32];
 #pragma unroll
   for (int v = 0; v < MODEL_MAX_BINS / 32; ++v) lg[v] = 0.f;
-  float bestE = -1.f;
-  int bestk = 0;
   for (int k = 1; k <= K; ++k) {
     const int64_t *dk = s_dur + (size_t)(k - 1) * (B + 1);
     if (!INTERP) {
@@ -94,26 +93,20 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __g
       for (int s = 0; s < p.nsteps; ++s) {
         const int64_t x = sig + p.off[s];
         float P;
+        // largest m in 0..B with dur[k][m] <= x (0 if none): branch-free
+        // binary search with a fixed trip count (rows non-decreasing in m)
+        int lo = 0;
+#pragma unroll
+        for (int st = MODEL_MAX_BINS; st > 0; st >>= 1)
+          if (lo + st <= B && dk[lo + st] <= x) lo += st;
         if (!INTERP) {
           // i* = #{m in 1..B : dur[k][m] <= x}  (A1: mass at the upper edges)
-          int lo = 0, hi = B;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (dk[mid] <= x) lo = mid;
-            else hi = mid - 1;
-          }
           P = lo == 0 ? 0.f : ex2_approx(stg[lo - 1]);
         } else {
           // largest m in 0..B with dur[k][m] <= x; position m + u inside the grid
           if (x < dk[0]) {
             P = 0.f;
           } else {
-            int lo = 0, hi = B;
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (dk[mid] <= x) lo = mid;
-              else hi = mid - 1;
-            }
             if (lo == B) {
               P = 1.f;
             } else {
@@ -131,19 +124,22 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __g
         acc = fmaf(p.dc[s], P, acc);
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    if (lane == 0) p.E[q * kmax + k - 1] = acc;
-    if (acc > bestE) {  // strict: ties -> smallest k
-      bestE = acc;
-      bestk = k;
-    }
+    part[(k - 1) * 33 + lane] = acc;  // reduced after the loop: no shuffle chain per k
     __syncwarp();
   }
+  // E_k in lane k-1: sum of the members' partials (lanes >= k contributed 0)
+  float E = 0.f;
+  if (lane < K)
+    for (int j = 0; j <= lane; ++j) E += part[lane * 33 + j];
   for (int k = K + 1 + lane; k <= kmax; k += 32) p.E[q * kmax + k - 1] = 0.f;
+  if (lane < K) p.E[q * kmax + lane] = E;
+  // argmax, ties -> smallest k (E >= 0: float bits order like values)
+  const uint32_t bits = lane < K ? __float_as_uint(E) : 0u;
+  const uint32_t mx = __reduce_max_sync(FULL, bits);
+  const uint32_t kb = __reduce_min_sync(FULL, (lane < K && bits == mx) ? (uint32_t)(lane + 1) : 0x7fffffffu);
   if (lane == 0) {
-    if (p.best_k) p.best_k[q] = bestk;
-    if (p.best_E) p.best_E[q] = bestk ? bestE : 0.f;
+    if (p.best_k) p.best_k[q] = K ? (int32_t)kb : 0;
+    if (p.best_E) p.best_E[q] = K ? __uint_as_float(mx) : 0.f;
   }
 }
 
