@@ -128,3 +128,27 @@ def test_segmented_arguments():
         orj.replay_trace(store, prof, tr, segments=0)
     with pytest.raises(orj.OrlojError, match="segments"):
         orj.replay_trace(store, prof, tr, segments=5000)
+
+
+@pytest.mark.parametrize("B", [16, 100])
+def test_segmented_other_bin_widths(B):
+    """Bins-per-lane variants 1 and 4 (the C5 families use 64 bins): random
+    histograms and a random bursty trace, segmented == plain."""
+    rng = np.random.default_rng(B)
+    D, S, n = 5, 12, 4000
+    counts = rng.integers(0, 50, size=(D, B)).astype(np.uint32)
+    counts[:, -1] += 1
+    store = orj.HistogramStore.from_counts(counts, 10)
+    kmax = 12
+    prof = orj.LatencyProfile(np.full(kmax, 40, np.int64), 2 + np.arange(kmax, dtype=np.int64) // 3)
+    gaps = rng.exponential(1.0, size=(S, n)) * rng.choice([5.0, 40.0, 400.0], size=(S, 1))
+    arr = (np.cumsum(gaps, axis=1).astype(np.int64) + (1 << 40)).reshape(-1)
+    dist = rng.integers(0, D, S * n).astype(np.int32)
+    tb = np.concatenate([rng.choice(np.flatnonzero(counts[d]) + 1, 1) for d in dist]).astype(np.int16)
+    off = np.arange(S + 1, dtype=np.int64) * n
+    slo = rng.integers(200, 3000, S).astype(np.int64)
+    tr = _trace(off, arr, dist, tb, slo)
+    for G in (3, 16):
+        pb0, log0, pb1, log1, pb2 = _both(store, prof, tr, G)
+        assert (pb1 == pb0).all() and (pb2 == pb0).all() and (log1 == log0).all(), G
+    assert pb0[:, 4].sum() > S  # scenarios actually batched
