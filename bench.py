@@ -772,15 +772,21 @@ def run_policies(args, rank, world, dev):
     thr = {f.tf.fam.name: torch.from_numpy(policy.expected_latency_thresholds(
         f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).to(dev) for f in fams}
     nb = len(gen.BUCKET_SLO_MULTS)
-    out = {"sweep": f"4 families x 8 buckets x {seeds} seeds x {args.replay_arrivals} arrivals"}
+    # segmented replay (same counters as the plain kernel, bit for bit), workspaces outside the timing
+    segs = [replay_segments(args.replay_segments, f.trace.num_scenarios, args.replay_arrivals) for f in fams]
+    wss = {f.tf.fam.name: torch.empty(max(orj.replay_seg_workspace_bytes(f.trace, g), 1), dtype=torch.uint8,
+                                      device=dev) for f, g in zip(fams, segs)}
+    out = {"sweep": f"4 families x 8 buckets x {seeds} seeds x {args.replay_arrivals} arrivals",
+           "segments_per_scenario": segs}
     for objective in ("expected_finish", "finish_rate"):
         for drop in ("hopeless", "expected_latency"):
             tabs = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for f, t_ in zip(fams, tabs):
+            for f, t_, g in zip(fams, tabs, segs):
                 orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, objective=objective,
-                                 drop_threshold=thr[f.tf.fam.name] if drop == "expected_latency" else None)
+                                 drop_threshold=thr[f.tf.fam.name] if drop == "expected_latency" else None,
+                                 segments=g, workspace=wss[f.tf.fam.name])
             e1.record()
             parallel.allreduce_counters(tabs)
             torch.cuda.synchronize()
@@ -801,9 +807,9 @@ def run_policies(args, rank, world, dev):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for f, t_, (pt, st) in zip(fams, tabs, setup):
+    for f, t_, (pt, st), g in zip(fams, tabs, setup, segs):
         orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, objective="alg1", priority=pt,
-                         size_thresholds=st)
+                         size_thresholds=st, segments=g, workspace=wss[f.tf.fam.name])
     e1.record()
     parallel.allreduce_counters(tabs)
     torch.cuda.synchronize()
