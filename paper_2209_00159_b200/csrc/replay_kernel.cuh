@@ -657,11 +657,12 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     float E = 0.f;
     if (mem) {
       const float4 *row = reinterpret_cast<const float4 *>(Pm + lane * PST);
+      const int nj = (wc + 3) >> 2;  // warp-uniform: quads holding members r < wc
       float acc[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         acc[j] = 0.f;
-        if (4 * j <= lane) {
+        if (j < nj && 4 * j <= lane) {
           const float4 x = row[j];
           acc[j] = (x.x + x.y) + (x.z + x.w);
         }
