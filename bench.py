@@ -462,6 +462,7 @@ def run_other_workloads(args, dev, max_over_ranks, world):
     out = {}
     stream = torch.cuda.Stream(dev)
     planner_k = None
+    c2_best_k = None
     for name, cfg, reps in (("C2", gen.config2(), 100), ("C4", gen.config4(), 1), ("C4-near", gen.config4(near=True), 1)):
         store = wl.score_store(cfg, dev)
         prof = wl.profile(cfg.profile)
@@ -497,16 +498,66 @@ def run_other_workloads(args, dev, max_over_ranks, world):
                      "us_per_pick": 1e3 * ms, "decisions_per_s": world * Q / (ms / 1e3),
                      "candidates_per_s": world * cands / (ms / 1e3),
                      "timing": f"{iters} x " + (f"CUDA graph of {reps} picks" if reps > 1 else "1 pick")}
+        if name == "C2":
+            c2_best_k = bk.cpu().numpy()
         if name == "C4":
             planner_k = bk.cpu().numpy()  # == the constant-latency planner, bit for bit (tests)
         if name == "C4-near" and planner_k is not None and len(planner_k) == Q:
             out[name]["agreement_with_planner"] = float((bk.cpu().numpy() == planner_k).mean())
         del store, qs
     torch.cuda.empty_cache()
+    out["C2-HBM"] = run_c2_hbm(dev, max_over_ranks, world, c2_best_k)
     out["C1_latency"] = run_c1_latency(dev)
     out["P1"] = run_priority(dev, max_over_ranks, world)
     out["C2_model_variants"] = run_model_variants(dev, max_over_ranks, world)
     return out
+
+
+def run_c2_hbm(dev, max_over_ranks, world, c2_best_k):
+    """C2-HBM: the C2 queues with one store row per request
+    (65,536 rows, 16.8 MB: the TMA row-ring path instead of the shared-memory
+    store), 100 picks per CUDA graph.  Each row equals its request's
+    application row, so k* must equal C2's bit for bit."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+
+    cfg = gen.config2()
+    q = cfg.queues
+    N = int(q.offsets[-1])
+    counts = np.ascontiguousarray(cfg.fam.counts[q.dist])             # [N][B]: request j's own row
+    store = orj.HistogramStore.from_counts(counts, cfg.fam.bin_ticks, dev)
+    qs = orj.Queues(wl.t(q.offsets, np.int64, dev), wl.t(q.deadline, np.int64, dev),
+                    wl.t(np.arange(N, dtype=np.int32), np.int32, dev), wl.t(q.now, np.int64, dev))
+    prof = wl.profile(cfg.profile)
+    bk = torch.empty(q.Q, dtype=torch.int32, device=dev)
+    bE = torch.empty(q.Q, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            orj.pick_batch(store, prof, qs, bk, bE, stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(100):
+            orj.pick_batch(store, prof, qs, bk, bE, stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / 2000
+    same = None if c2_best_k is None else bool((bk.cpu().numpy() == c2_best_k).all())
+    K = np.minimum(np.diff(q.offsets), cfg.kmax)
+    return {"workload": "C2 queues (1,024 x 64, kmax 32, B 64) over 65,536 per-request rows (16.8 MB store)",
+            "us_per_pick": 1e3 * ms, "decisions_per_s": world * q.Q / (ms / 1e3),
+            "row_bytes_per_pick": int(K.sum()) * cfg.fam.B * 4, "best_k_equals_C2": same,
+            "timing": "20 x CUDA graph of 100 picks; the 16.8 MB store stays in L2 between picks"}
 
 
 def run_c1_latency(dev):
