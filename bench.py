@@ -757,6 +757,9 @@ def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
     return int(max(1, min(g, n_arr // 2000, 4096)))
 
 
+REPLAY_SWEEP_WARP_INSTR = 87_906_266_861  # ncu, full C5 sweep at 8 segments (profiles/r01_replay_sweep_n1_launches.csv)
+
+
 def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True, segments="auto"):
     """One sweep = the 4 family replays on 4 streams + one all-reduce of the
     [4 x 8 x 7] int64 counters (NCCL; a no-op on one rank), all inside the
@@ -899,6 +902,17 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
            "gpu_launches_per_sweep": sum(2 if g > 1 else 1 for g in segs), "clocks": clk,
            "collective": "one torch.distributed.all_reduce of the int64 [4 x 8 x 7] counters (NCCL) per sweep, "
                          "inside the timed region"}
+    if (world == 1 and segs == [8, 8, 8, 8] and args.replay_seeds == 256
+            and args.replay_arrivals == 100_000):
+        # issue roofline of the full 1-GPU sweep: the warp-instruction count is a
+        # property of the (deterministic) workload, counted once by ncu
+        # (profiles/r01_replay_sweep_n1_launches.csv: smsp__inst_executed.sum of
+        # the 8 launches of one sweep); the time is this run's
+        peak = 148 * 4 * clk.get("sm_max_mhz", 1965) * 1e6 / 1e12     # 4 schedulers x 1 warp-instr/cycle per SM
+        achieved = REPLAY_SWEEP_WARP_INSTR / (ms / 1e3) / 1e12
+        out["roofline"] = {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "T warp-instructions/s",
+                           "frac": achieved / peak, "instructions_per_sweep": REPLAY_SWEEP_WARP_INSTR,
+                           "peak_source": "148 SMs x 4 warp schedulers x 1 instruction/cycle at sm_max_mhz"}
     if not args.no_policies:
         out["policies"] = run_policies(args, rank, world, dev)
     if world == 1 and not args.no_shard_proxy:
