@@ -400,6 +400,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         }
         __syncwarp();
         seg_end = seg_begin(n, g + 2, p.G);
+        // every extension iteration starts below s_{g+2}, which bounds the
+        // scratch log (seg_log_off); a run already past it has no extension
+        if (cursor >= seg_end) break;
       }
       if (cursor >= rec_at && ncarry == 0) {
         const int64_t a0 = __shfl_sync(FULL, ua, 0);
