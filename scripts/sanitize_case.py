@@ -36,6 +36,7 @@ def main():
     # segmented replay (speculative segments + stitch), with and without the log
     orj.replay_trace(f.store, f.profile, f.trace, decision_log=True, segments=5)
     orj.replay_trace(f.store, f.profile, f.trace, segments=3, objective="finish_rate")
+    orj.replay_trace(f.store, f.profile, f.trace, decision_log=True, segments=200)  # segments of 2-3 arrivals
     # Alg. 1 policy (priority tables inside the replay kernel)
     from paper_2209_00159_b200 import policy
     pt = orj.PriorityTable(f.store, f.profile, f.profile.kmax, 1.0 / f.tf.fam.mean_ticks())
