@@ -62,3 +62,23 @@ def test_invariants_point_masses():
     c = gen.config4(Q=300)
     _check(wl.score_store(c), wl.profile(c.profile), wl.device_queues(c.queues), np.diff(c.queues.offsets), c.kmax,
            point_mass=True)
+
+
+def test_determinism():
+    """T5: reruns on the same inputs are byte-identical (pick, score with
+    P, segmented replay with its log)."""
+    c = gen.config2(Q=300)
+    store, prof, qs = wl.score_store(c), wl.profile(c.profile), wl.device_queues(c.queues)
+    runs = []
+    for _ in range(2):
+        bk, bE = orj.pick_batch(store, prof, qs)
+        sc = orj.score_batches(store, prof, qs, want_P=True, want_EL=True)
+        runs.append([bk.cpu().numpy(), bE.cpu().numpy()] + [sc[k].cpu().numpy() for k in ("E", "P", "EL")])
+    for a, b in zip(*runs):
+        assert a.tobytes() == b.tobytes()
+    fam = wl.C5Family("rdi", local_ids=np.arange(24), n_arr=8000)
+    logs = []
+    for _ in range(2):
+        pb, log = orj.replay_trace(fam.store, fam.profile, fam.trace, decision_log=True, segments=9)
+        logs.append((pb.cpu().numpy().tobytes(), log.cpu().numpy().tobytes()))
+    assert logs[0] == logs[1]
