@@ -77,6 +77,31 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`--gpus N > 1` outside torchrun: re-run this command as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1), the
+    launch the driver uses.  N must not exceed the visible GPUs unless
+    ORLOJ_BENCH_SHARE_GPU=1 (functional check: every rank on cuda:0, gloo)."""
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if args.gpus > have and os.environ.get("ORLOJ_BENCH_SHARE_GPU") != "1":
+        print(json.dumps({"error": f"--gpus {args.gpus} but only {have} GPU(s) visible",
+                          "hint": "run on a box with enough GPUs (or ORLOJ_BENCH_SHARE_GPU=1 for a functional "
+                                  "check with every rank on cuda:0)"}), flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------------------
 # clocks sampled during the timed region (NVML)
 # ----------------------------------------------------------------------------
@@ -256,6 +281,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -278,6 +305,11 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        comm = {"backend": dist.get_backend(), "world_size": world, "local_rank_device": local,
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if not shared else None,
+                "shared_gpu_functional_check": shared}
 
     def barrier():
         if world > 1:
@@ -364,6 +396,8 @@ def main():
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
+    if comm:
+        result["comm"] = comm
     if args.ncu:
         if rank == 0:
             print(json.dumps(result), flush=True)
@@ -916,18 +950,35 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
     if not args.no_policies:
         out["policies"] = run_policies(args, rank, world, dev)
     if world == 1 and not args.no_shard_proxy:
-        # strong-scaling proxy on one GPU: the time of rank 0's shard of an N-GPU run
-        # (everything but the ~10 us all-reduce), and the implied speed-up
+        # strong-scaling proxy on one GPU: time EVERY rank's shard of an N-GPU run
+        # (median of 3 sweeps each; everything but the ~10 us all-reduce) and take
+        # the max over ranks, as a real N-GPU run would
         del fams
-        proxy = {}
-        for N in (2, 4, 8):
-            sf = build_replay(args, 0, N, dev)
-            sms, stabs, _ = time_replay(sf, 1, dev, lambda: None, lambda x: x, reduce=False,
+        out["shard_proxy"] = shard_proxy(args, dev, ms)
+    return out
+
+
+def shard_proxy(args, dev, ms_full):
+    proxy = {"method": "each rank's round-robin shard replayed alone on this GPU, median of 3 sweeps; "
+                       "implied speed-up = full sweep / max over ranks (not a measured N-GPU run)"}
+    for N in (2, 4, 8):
+        per_rank = []
+        segs = None
+        for r in range(N):
+            sf = build_replay(args, r, N, dev)
+            ts = []
+            for _ in range(3):
+                sms, _, _ = time_replay(sf, 1, dev, lambda: None, lambda x: x, reduce=False,
                                         segments=args.replay_segments)
-            proxy[str(N)] = {"ms_rank0_shard": sms, "implied_speedup": ms / sms,
-                             "segments_per_scenario": list(time_replay.segments)}
+                ts.append(sms)
+            per_rank.append(float(np.median(ts)))
+            segs = list(time_replay.segments)
             del sf
-        out["shard_proxy"] = proxy
+        mx = max(per_rank)
+        proxy[str(N)] = {"ms_per_rank": [round(x, 3) for x in per_rank], "ms_max_over_ranks": mx,
+                         "ms_min_over_ranks": min(per_rank), "imbalance": mx / min(per_rank),
+                         "implied_speedup": ms_full / mx, "segments_per_scenario": segs}
+    return proxy
     return out
 
 

@@ -274,10 +274,13 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
  * may then be NULL).  num_arrivals: arrival_offsets[S] (sizes the workspace).
  * workspace: caller-owned, 256-byte aligned device memory of at least
  * orloj_replay_seg_workspace(S, num_arrivals, segments, decision_log != NULL)
- * bytes; contents are scratch except its first 32 bytes, which hold int64
+ * bytes; contents are scratch except its first 40 bytes, which hold int64
  * diagnostics of the call once it completes: {decisions the second pass re-ran,
  * segments joined at a common regeneration point, segments run through,
- * decisions the first pass made past the segment ends}.
+ * decisions the first pass made past the segment ends, size error}.  The
+ * workspace is sized from num_arrivals: if arrival_offsets[S] exceeds it the
+ * kernels do nothing (counters and log untouched) and set the size-error word
+ * to 1 (the check needs the device offsets, so it cannot be synchronous).
  * policy: as orloj_replay_trace_ex (NULL: the
  * default expected-finish policy).  Errors: INVALID_ARGUMENT for a bad segment
  * count or a missing / short / misaligned workspace, else as

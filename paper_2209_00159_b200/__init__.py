@@ -424,6 +424,11 @@ class Trace:
         _dev(self.true_bin, torch.int16, "true_bin")
         _dev(self.slo, torch.int64, "slo")
         _dev(self.bucket, torch.int32, "bucket")
+        if self.offsets.numel() != self.slo.numel() + 1:
+            raise OrlojError(1, "offsets must have num_scenarios + 1 entries")
+        # the segmented replay sizes its scratch from num_arrivals = arrival.numel()
+        if self.slo.numel() > 0 and int(self.offsets[-1]) != self.arrival.numel():
+            raise OrlojError(1, "offsets[-1] must equal the number of arrivals")
         self._c = _abi.TraceC(self.slo.numel(), self.offsets.data_ptr(), self.arrival.data_ptr(),
                               self.dist.data_ptr(), self.true_bin.data_ptr(), self.slo.data_ptr(),
                               self.bucket.data_ptr(), int(self.num_buckets))
@@ -507,8 +512,9 @@ def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, p
 
 def replay_seg_stats(workspace: torch.Tensor) -> dict:
     """Diagnostics a completed segmented replay left in its workspace head."""
-    v = workspace[:32].view(torch.int64).cpu().tolist()
-    return {"stitch_decisions": v[0], "joined": v[1], "crossed": v[2], "extension_decisions": v[3]}
+    v = workspace[:40].view(torch.int64).cpu().tolist()
+    return {"stitch_decisions": v[0], "joined": v[1], "crossed": v[2], "extension_decisions": v[3],
+            "size_error": v[4]}
 
 
 def replay_seg_workspace_bytes(trace: Trace, segments: int, with_log: bool = False) -> int:

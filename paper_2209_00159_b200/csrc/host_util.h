@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 
@@ -22,6 +23,21 @@ orloj_status compile_profile(const orloj_latency_profile *pr, int32_t B, int kca
 orloj_status check_queues(const orloj_queues *q);
 int bins_per_lane(int B);
 int slots_for(int kmax);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device property of a
+// kernel: set it once per (kernel, device) — `done` is one bit per device id
+// (ids >= 64 set it on every call).  Idempotent, so a race only repeats it.
+template <class K>
+cudaError_t ensure_max_dyn_smem(K kernel, int bytes, std::atomic<uint64_t> &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 }  // namespace host
 }  // namespace orloj

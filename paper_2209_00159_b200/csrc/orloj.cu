@@ -168,13 +168,9 @@ template <bool SMEM_TABLE, bool STEPS>
 cudaError_t prio_launch(unsigned grid, size_t smem, cudaStream_t s, const double *log_table,
                         const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
                         const StepsDev &steps, const orloj_queues *q, float *out) {
-  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
-  if (!configured.load(std::memory_order_acquire)) {
-    const cudaError_t e = cudaFuncSetAttribute(priority_scores_kernel<SMEM_TABLE, STEPS>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_release);
-  }
+  static std::atomic<uint64_t> configured{0};  // per instantiation and device
+  const cudaError_t e = ensure_max_dyn_smem(priority_scores_kernel<SMEM_TABLE, STEPS>, 96 << 10, configured);
+  if (e != cudaSuccess) return e;
   priority_scores_kernel<SMEM_TABLE, STEPS><<<grid, 256, smem, s>>>(log_table, log_expected, S, B, b, prof, steps,
                                                                     q->num_queues, q->queue_offsets,
                                                                     q->deadline_ticks, q->now_ticks, out);

@@ -73,8 +73,9 @@ struct ReplayParams {
   int32_t G;                      // segments per scenario
   struct ReplaySeg *seg;          // [S][G]
   int32_t *seg_log;               // scratch decision logs of segments g >= 1 (MODE 1 with a log)
-  unsigned long long *seg_stats;  // [4]: decisions re-run by the stitch, segments joined, segments crossed,
-                                  //      decisions in the extensions
+  unsigned long long *seg_stats;  // [5]: decisions re-run by the stitch, segments joined, segments crossed,
+                                  //      decisions in the extensions, inconsistent-size flag (zeroed by the host)
+  int64_t num_arrivals;           // MODE 1 / 2: the caller's arrival_offsets[S] (sizes seg_log)
 };
 
 constexpr int SEG_REC = 20;  // regeneration points recorded per list
@@ -189,8 +190,14 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   if (lane < REPLAY_KB) stg[lane * STG - 1] = -INFINITY;
   __syncthreads();
 
-  if constexpr (MODE == 1)
-    if (blockIdx.x == 0 && threadIdx.x < 4) p.seg_stats[threadIdx.x] = 0;  // read after this launch only
+  if constexpr (MODE != 0) {
+    // the scratch logs are sized from the caller's num_arrivals: a trace with
+    // more arrivals would write past them — refuse the whole call, flag it
+    if (p.arr_off[p.S] - p.arr_off[0] > p.num_arrivals) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.seg_stats[4] = 1;
+      return;
+    }
+  }
   const int64_t u = (int64_t)blockIdx.x * REPLAY_WARPS + wid;
   int64_t s = u;
   int g = 0;  // MODE 1: this warp's segment; MODE 2: the segment being stitched

@@ -27,13 +27,9 @@ cudaError_t launch_score_t(const ScoreParams &p, cudaStream_t s) {
   const size_t base = ScoreShape<BPL>::smem_bytes();
   const size_t smem = base + (SMEMS ? (size_t)p.D * p.B * 4 : 0);
   const size_t cap = base + (SMEMS ? (size_t)SMEM_STORE_BYTES : 0);
-  static std::atomic<bool> configured{false};  // per instantiation; idempotent attribute
-  if (!configured.load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_release);
-  }
+  static std::atomic<uint64_t> configured{0};  // per instantiation and device
+  cudaError_t e = ensure_max_dyn_smem(score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS>, (int)cap, configured);
+  if (e != cudaSuccess) return e;
   score_kernel<BPL, SLOTS, PICK, STREAM, SMEMS><<<(unsigned)blocks, SCORE_WARPS * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
@@ -61,14 +57,10 @@ template <int BPL, bool PICK>
 cudaError_t launch_score_small(const ScoreParams &p, cudaStream_t s) {
   const int64_t blocks = (p.Q + SMALL_WARPS - 1) / SMALL_WARPS;
   const size_t smem = SmallShape<BPL>::bytes(p.D, p.B);
-  static std::atomic<bool> configured{false};
-  if (!configured.load(std::memory_order_acquire)) {
-    const size_t cap = SmallShape<BPL>::bytes((int)(SMEM_STORE_BYTES / (32 * BPL * 4)), 32 * BPL);
-    cudaError_t e = cudaFuncSetAttribute(score_small_kernel<BPL, PICK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)cap);
-    if (e != cudaSuccess) return e;
-    configured.store(true, std::memory_order_release);
-  }
+  static std::atomic<uint64_t> configured{0};
+  const size_t cap = SmallShape<BPL>::bytes((int)(SMEM_STORE_BYTES / (32 * BPL * 4)), 32 * BPL);
+  cudaError_t e = ensure_max_dyn_smem(score_small_kernel<BPL, PICK>, (int)cap, configured);
+  if (e != cudaSuccess) return e;
   score_small_kernel<BPL, PICK><<<(unsigned)blocks, SMALL_WARPS * 32, smem, s>>>(p);
   return cudaGetLastError();
 }

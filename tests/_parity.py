@@ -56,3 +56,42 @@ def check_P(P_gpu, P_or, lens, kmax):
     assert err.size == 0 or err.max() <= P_TOL, f"max P err {err.max()}"
     assert (P_gpu[valid] >= 0).all() and (P_gpu[valid] <= 1).all()
     return 0.0 if err.size == 0 else err.max()
+
+
+def record(kind: str, **stats):
+    """Append a parity statistic (e.g. tie counts) as one JSON line to the file
+    named by $ORLOJ_PARITY_LOG (evidence for DESIGN.md); no-op otherwise."""
+    import json
+    import os
+    path = os.environ.get("ORLOJ_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"kind": kind, **{k: (v.item() if hasattr(v, "item") else v)
+                                                 for k, v in stats.items()}}) + "\n")
+
+
+def check_replay_follow(ref, counters_gpu, label: str, tie_rate: float = 1e-5, free=None, log_gpu=None):
+    """Replay parity in follow mode: every GPU decision lies in
+    the oracle's tie set, the integer counters are bit-exact, and the number of
+    GPU choices that differ from the oracle's own choice (documented ties) is
+    reported and bounded by `tie_rate` x decisions (+1 for a lone tie in a
+    tiny case).  With the oracle's free run `free`, every scenario without a
+    differing decision must equal it bit for bit (counters, and the log when
+    both logs are given): the free run can only diverge after a tie."""
+    ties = ref["ties"]
+    bad = np.nonzero(ties[:, 2] != -1)[0]
+    assert bad.size == 0, f"{label}: scenario {bad[:5]} has a GPU decision outside the oracle tie set"
+    assert (ref["counters"] == counters_gpu).all(), f"{label}: counters differ in follow mode"
+    dec, diff = int(ties[:, 0].sum()), int(ties[:, 1].sum())
+    clean = ties[:, 1] == 0
+    out = {"decisions": dec, "differing_choices": diff, "scenarios": len(ties),
+           "scenarios_with_ties": int((~clean).sum())}
+    if free is not None:
+        same = (free["counters"] == counters_gpu).all(1)
+        assert same[clean].all(), f"{label}: a tie-free scenario differs from the oracle's free run"
+        out["free_run_identical_scenarios"] = int(same.sum())
+        if log_gpu is not None and free.get("log") is not None and clean.all():
+            assert (free["log"] == log_gpu).all(), f"{label}: free-run log differs"
+    record("replay_ties", label=label, **out)
+    assert diff <= tie_rate * dec + 1, f"{label}: {diff} differing choices in {dec} decisions"
+    return out

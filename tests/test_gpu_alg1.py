@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import gen
+import _parity as par
 from oracle import alg1
 
 torch = pytest.importorskip("torch")
@@ -77,4 +78,6 @@ def test_follow_mode_parity(name):
     assert (ref["ties"][:, 2] == -1).all(), ref["ties"]
     assert np.array_equal(ref["counters"], pb)  # one scenario per bucket
     # the popped sets differ from the oracle's own choice only at near-ties
+    par.record("replay_ties", label=f"alg1/{name}", decisions=int(ref["ties"][:, 0].sum()),
+               differing_choices=int(ref["ties"][:, 1].sum()), scenarios=nb)
     assert ref["ties"][:, 1].sum() <= 0.01 * ref["ties"][:, 0].sum() + 2

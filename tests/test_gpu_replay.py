@@ -14,6 +14,7 @@ import pytest
 
 import gen
 import oracle
+import _parity as par
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -49,14 +50,12 @@ def test_replay_follow_mode(fam):
     pb, log = _gpu_replay(store, prof, off, arr, dist, tb, slo)
     F = oracle.cdf(tf.fam.counts)
     ref = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo, follow_log=log)
-    assert (ref["ties"][:, 2] == -1).all(), "a GPU decision lies outside the oracle tie set"
-    assert (pb == ref["counters"]).all()
+    free = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo, want_log=True)
+    st = par.check_replay_follow(ref, pb, f"C5-20k/{fam}", free=free, log_gpu=log)
     c = pb
     assert (c[:, 1] + c[:, 2] + c[:, 3] == c[:, 0]).all()
-    free = oracle.replay(F, tf.profile.a, tf.profile.w, off, arr, dist, tb, slo, want_log=True)
-    same = (free["counters"] == pb).all(1).mean()
-    assert same >= 0.9, same
-    if fam == "static":
+    if fam == "static":   # integer-valued E_k: no near-ties at all
+        assert st["differing_choices"] == 0
         assert (free["counters"] == pb).all() and (free["log"] == log).all()
 
 
