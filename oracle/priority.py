@@ -149,6 +149,68 @@ def scores_steps(counts, a, w, num_sizes, b, offsets, deadline, now, step_offset
     return out
 
 
+def store_rounding_eta(counts) -> np.ndarray:
+    """eta_i >= |F^_d(tau_i) / F_d(tau_i) - 1| for every application d, where
+    F^ = 2^{fl32(log2 F)} is F read through the store format (one RN rounding
+    of log2 F to fp32: |dx| <= 2^-24 |x|, plus 2^-20 of that for a last-place
+    error of the fp64 log2 before it): eta = e^{ln 2 * 2^-24 (1 + 2^-20) |log2 F|} - 1.
+    F = 0 and F = 1 are exact (-inf and 0.0f), so they contribute 0; bin B is
+    forced to 1 on both sides."""
+    c = np.asarray(counts, dtype=np.float64)
+    F = np.cumsum(c, axis=1) / c.sum(axis=1, keepdims=True)
+    with np.errstate(divide="ignore"):
+        x = np.abs(np.log2(F))
+    x[~np.isfinite(x)] = 0.0
+    eta = np.expm1(np.log(2.0) * 2.0 ** -24 * (1 + 2.0 ** -20) * x).max(axis=0)
+    eta[-1] = 0.0
+    return eta
+
+
+def store_rounding_log_priority_bound(counts, a, w, b, sigma, bs, weights=None) -> np.ndarray:
+    """First-order bound on |log p(F^) - log p(F)| for one batch size: how far
+    the store format alone (log2 F rounded once to fp32) can move the Eq. 2
+    priority of the exact histogram model.  The mixture CDF moves by at most
+    eta_i relatively (a weighted mean of per-application factors), G_i = F^bs
+    by gamma_i = G_i ((1 + eta_i)^bs - 1), a bin mass pm_i = G_i - G_{i-1} by
+    dpm_i = gamma_i + gamma_{i-1}.  With T_i(sigma) >= 0 the per-unit-mass
+    Eq. 2 term of bin i, p E[L] = sum pm_i T_i moves by at most
+    r = sum dpm_i T_i / sum pm_i T_i relatively and E[L] = sum pm_i mid_i by
+    r_L = sum dpm_i mid_i / E[L]; |d log p| <= r/(1-r) + r_L/(1-r_L)
+    (|log(1+d)| <= |d|/(1-|d|)).  inf where r >= 1 (bins whose mass the
+    rounding may erase decide p: near-empty bins at large bs)."""
+    F = mixture_cdf(counts, weights)
+    F[-1] = 1.0
+    eta = store_rounding_eta(counts)
+    G = F ** bs
+    gam = G * np.expm1(bs * np.log1p(eta))
+    dpm = gam + np.concatenate([[0.0], gam[:-1]])
+    lpm = batch_latency_logpmf(counts, bs, weights)
+    pm = np.exp(lpm)
+    sig = np.atleast_1d(np.asarray(sigma, dtype=np.float64))
+    B = len(pm)
+    i = np.arange(1, B + 1, dtype=np.float64)
+    EL = float(np.sum(pm * (a + w * (i - 0.5))))
+    rL = float(np.sum(dpm * (a + w * (i - 0.5)))) / EL
+    lnum = np.full(sig.shape, -np.inf)      # log sum dpm_k T_k, log domain (e^{-b sigma} underflows)
+    lden = np.full(sig.shape, -np.inf)      # log sum pm_k T_k
+    with np.errstate(divide="ignore"):
+        ldpm = np.log(dpm)
+    for k in range(1, B + 1):
+        l1, l2 = a + w * (k - 1), a + w * k
+        lT = np.full(sig.shape, -np.inf)
+        full = sig >= l2
+        part = (sig > l1) & (sig < l2)
+        lT[full] = -b * (sig[full] - l2) + np.log(-np.expm1(-b * w)) - np.log(w * b)
+        lT[part] = np.log(-np.expm1(-b * (sig[part] - l1))) - np.log(w * b)
+        lnum = np.logaddexp(lnum, ldpm[k - 1] + lT)
+        lden = np.logaddexp(lden, lpm[k - 1] + lT)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.where(np.isfinite(lden), np.exp(lnum - lden), np.inf)
+        out = r / (1.0 - r) + rL / (1.0 - rL)
+    out[~(r < 1.0)] = np.inf
+    return out
+
+
 def pop_batch(logp_rows, bs, num_sizes, cap=256) -> list[int]:
     """PopBatch (Alg. 1 line 18): the (up to) bs members with the highest
     priority for size bs, highest first, ties to the earlier member, members

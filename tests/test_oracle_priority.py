@@ -214,3 +214,99 @@ def test_batch_logpmf_exact_rationals_beyond_fp64_range(bs):
         else:
             want = math.log(pm.numerator) - math.log(pm.denominator)
             assert abs(got[i] - want) <= 1e-12 * max(1.0, abs(want)), (i, got[i], want)
+
+
+# ---------------------------------------------------------------------------
+# the store-format branch (store_fp32=True) and its distance to the exact model
+# ---------------------------------------------------------------------------
+
+def _rn_f32_of_log2(num: int, den: int):
+    """fl32(log2(num/den)) by RN, decided in exact arithmetic: log2 to 60
+    decimal digits (decimal module, independent of numpy's log2), then the
+    nearest float32 among the candidates around it."""
+    from decimal import Decimal, getcontext
+    from fractions import Fraction
+    getcontext().prec = 60
+    if num == den:
+        return np.float32(0.0), Fraction(1)       # log2 1 = 0 exactly
+    x = (Decimal(num) / Decimal(den)).ln() / Decimal(2).ln()
+    xf = Fraction(x)
+    c = np.float32(float(x))
+    cands = [c, np.nextafter(c, np.float32(-np.inf)), np.nextafter(c, np.float32(np.inf))]
+    dist = [abs(Fraction(float(v)) - xf) for v in cands]
+    best = cands[int(np.argmin(dist))]
+    gap = sorted(dist)[1] - sorted(dist)[0]     # distance from a rounding midpoint (x2)
+    return best, gap / abs(xf)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mixture_cdf_store_fp32_is_the_rounded_model(seed):
+    """mixture_cdf(store_fp32=True) is the mixture of F^_d = 2^{RN32(log2 F_d)}
+    (the store's data format, include/orloj.h): checked against the RN
+    rounding decided in exact arithmetic and 2^x evaluated with 60-digit
+    decimals, with weights, on rows with empty bins, near-1 CDFs (single-count
+    tails at total 2^30, where the rounding erases masses) and exact powers
+    of two (log2 F an integer)."""
+    from decimal import Decimal, getcontext
+    from fractions import Fraction
+    getcontext().prec = 60
+    rng = np.random.default_rng(gen.SEED_BASE + 930 + seed)
+    D, B = 4, 12
+    counts = np.zeros((D, B), np.int64)
+    counts[0] = rng.integers(0, 50, B)
+    counts[0, 3] += 1
+    counts[1] = gen.largest_remainder(rng.dirichlet(np.ones(B)))        # total 2^30
+    counts[2, :] = 0
+    counts[2, 1], counts[2, 5], counts[2, 11] = 1 << 28, (1 << 30) - (1 << 28) - 3, 3   # F = 1/4 exactly; tails
+    counts[3, 0], counts[3, B - 1] = (1 << 30) - 1, 1
+    weights = [0.5, 2.0, 1.0, 0.25] if seed else None
+    got = pr.mixture_cdf(counts, weights, store_fp32=True)
+    wts = [Fraction(1)] * D if weights is None else [Fraction(x) for x in weights]
+    cum = np.cumsum(counts, axis=1)
+    tot = counts.sum(axis=1)
+    for i in range(B):
+        acc = Fraction(0)
+        for d in range(D):
+            if cum[d, i] == 0:
+                continue                            # F = 0: log2 = -inf exactly, 2^-inf = 0
+            x32, rel_gap = _rn_f32_of_log2(int(cum[d, i]), int(tot[d]))
+            assert rel_gap > 2.0 ** -40, "too close to a rounding midpoint to decide"
+            assert np.float32(np.log2(cum[d, i] / tot[d])) == x32      # numpy's path rounds the same way
+            acc += wts[d] * Fraction(Decimal(2) ** Decimal(float(x32)))
+        ref = acc / sum(wts)
+        assert abs(got[i] - float(ref)) <= 4e-16 * float(ref) + 1e-300, (i, got[i], float(ref))
+    # F = 1/4 exactly survives the rounding exactly; the tail masses of row 3 vanish
+    assert pr.mixture_cdf(counts[2:3], store_fp32=True)[1] == 0.25
+    F3 = pr.mixture_cdf(counts[3:4], store_fp32=True)
+    assert F3[0] < 1.0 and F3[B - 1] == 1.0
+
+
+def test_store_rounding_bound_holds():
+    """The first-order bound on how far the store format moves log p from the
+    exact histogram model (store_rounding_log_priority_bound) covers the
+    actual difference between the two oracle branches on every workload
+    family, batch size and slack.  Within e^10 of the size's largest priority
+    it stays below 1e-2 (largest: the RDI-like family, a few 1e-3).  Far
+    below that it grows and is infinite where p is decided by bins whose mass
+    the rounding may erase (near-empty bins at the start of L_bs's support;
+    RDI-like at b = 20 / mean: log p more than 20 below the maximum), which
+    the tests report rather than bound."""
+    fams = [("P1", gen.config_priority())] + [(f, gen.c5_trace_family(f)) for f in gen.C5_FAMILIES]
+    for name, cfg in fams:
+        counts, a, w = cfg.fam.counts, cfg.profile.a, cfg.profile.w
+        for b in (0.05 / cfg.fam.mean_ticks(), 1.0 / cfg.fam.mean_ticks(), 20.0 / cfg.fam.mean_ticks()):
+            for bs in (1, 2, 5, 16, 32):
+                if bs > len(a):
+                    continue
+                ak, wk = float(a[bs - 1]), float(w[bs - 1])
+                sig = np.linspace(-100.0, (ak + wk * counts.shape[1]) * 1.3, 1500)
+                p0 = pr.log_priority_lp(pr.batch_latency_logpmf(counts, bs), ak, wk, b, sig)
+                p1 = pr.log_priority_lp(pr.batch_latency_logpmf(counts, bs, store_fp32=True), ak, wk, b, sig)
+                assert (np.isneginf(p0) == np.isneginf(p1)).all()
+                fin = np.isfinite(p0)
+                bound = pr.store_rounding_log_priority_bound(counts, ak, wk, b, sig, bs)
+                relevant = fin & (p0 >= p0[fin].max() - 10.0)
+                assert np.isfinite(bound[relevant]).all(), (name, bs, b)
+                fb = fin & np.isfinite(bound)
+                assert bound[relevant].max() < 1e-2, (name, bs)
+                assert (np.abs(p0[fb] - p1[fb]) <= bound[fb]).all(), (name, bs, b)
