@@ -483,3 +483,47 @@ def trace_host(tf: TraceFamily, gids, n_arr: int):
     _host_lib().gen_trace_host(tf.seed, _ptr(gids), S, n_arr, _ptr(tf.exp_q16), tf.base_gap, tf.fam.D,
                                _ptr(np.ascontiguousarray(tf.cum)), tf.fam.B, T0, _ptr(arr), _ptr(dist), _ptr(tb))
     return arr, dist, tb
+
+
+# ----------------------------------------------------------------------------
+# feedback-loop workload: input drift + profiler sampling
+# ----------------------------------------------------------------------------
+
+def drifted_trace_family(tf: TraceFamily, slow_apps: int | None = None, num: int = 3, den: int = 2) -> TraceFamily:
+    """The same arrival process and applications, but the first `slow_apps`
+    applications (default: half) run num/den times slower: bin i's mass moves
+    to bin min(B, ceil(i num / den)) (integer remap, totals unchanged).  Its
+    traces differ from tf's only in the true bins (gen_true_bin reads only
+    `cum`), so a drifted trace is the base trace with later true bins swapped
+    in (PAPER.md:385-387: "arrival pattern ... change over time")."""
+    import dataclasses
+    D, B = tf.fam.counts.shape
+    slow = D // 2 if slow_apps is None else slow_apps
+    c = tf.fam.counts.astype(np.int64).copy()
+    for d in range(slow):
+        row = np.zeros(B, np.int64)
+        for i in range(1, B + 1):
+            row[min(B, -(-i * num // den)) - 1] += c[d, i - 1]
+        c[d] = row
+    fam = dataclasses.replace(tf.fam, name=tf.fam.name + "-drift", counts=c.astype(np.uint32))
+    return dataclasses.replace(tf, fam=fam, cum=fam.cum())
+
+
+def drift_trace_host(tf: TraceFamily, gids, n_arr: int, num_epochs: int, drift_epoch: int):
+    """Base trace of tf whose true bins from epoch `drift_epoch` on (epoch e of a
+    scenario = arrivals [floor(e n / E), floor((e+1) n / E))) come from the
+    drifted family.  Returns (arrival, dist, true_bin, drifted TraceFamily)."""
+    arr, dist, tb = trace_host(tf, gids, n_arr)
+    tfd = drifted_trace_family(tf)
+    _, dist2, tb2 = trace_host(tfd, gids, n_arr)
+    assert (dist2 == dist).all()
+    j0 = (drift_epoch * n_arr) // num_epochs
+    tb = tb.reshape(-1, n_arr)
+    tb[:, j0:] = tb2.reshape(-1, n_arr)[:, j0:]
+    return arr, dist, tb.reshape(-1), tfd
+
+
+def sample_mask(seed: int, n: int, rate: float) -> np.ndarray:
+    """The profiler's sample of completed requests ("finished
+    requests are sampled"): uint8 [n], 1 with probability `rate` (seeded)."""
+    return (np.random.default_rng(seed).random(n) < rate).astype(np.uint8)

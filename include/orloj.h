@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define ORLOJ_ABI_VERSION 3
+#define ORLOJ_ABI_VERSION 4
 #define ORLOJ_MAX_KMAX 256        /* candidate batch sizes per queue (score / pick) */
 #define ORLOJ_MAX_BINS 256        /* bins per histogram (score / pick) */
 #define ORLOJ_REPLAY_MAX_KMAX 32  /* window size in replay */
@@ -293,6 +293,75 @@ orloj_status orloj_replay_trace_seg(const orloj_store *store, const orloj_latenc
                                     int32_t segments, int64_t num_arrivals, void *workspace,
                                     size_t workspace_bytes, orloj_counters *per_bucket,
                                     int32_t *decision_log, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Long-term feedback loop: "finished
+ * requests are sampled and sent to the profiler to evaluate individually. The
+ * execution time data will then be asynchronously picked up and accumulated
+ * by the scheduler periodically ... resets its profiling memory every once in
+ * a while."  Reading R15: a replay is cut into epochs; the
+ * store is static during an epoch (A18); at the end of an epoch the sampled
+ * completed requests' solo times (their hidden true bins) are added to the
+ * profiling window, every row whose window holds >= min_samples samples is
+ * rebuilt, and the window is reset every window_epochs epochs.  An epoch
+ * boundary is a batching barrier (an epoch's arrivals are all handled before
+ * the next epoch's are admitted); the worker's busy time carries over.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t epoch;              /* 0 <= epoch < num_epochs */
+  int32_t num_epochs;         /* >= 1: epoch e of scenario s = its arrivals [s_e, s_{e+1}), s_e = floor(e n_s / num_epochs) */
+  int64_t *worker_free_ticks; /* device int64 [S] or NULL: read at the start (the worker is busy until then;
+                                 INT64_MIN = free), overwritten with the end of the scenario's last batch */
+  uint8_t *outcome;           /* device uint8 [N] or NULL: every arrival of the epoch gets 1 (finished),
+                                 2 (late) or 3 (dropped); other entries are untouched */
+} orloj_replay_epoch;
+/* orloj_replay_trace_ex over one epoch (plain kernel).  Counters count the
+ * epoch's arrivals (span_ticks = end of its last batch - its first arrival).
+ * decision_log: device int32 [N + S] or NULL; decision d of the epoch of
+ * scenario s at [arrival_offsets[s] + s + s_e + d], followed by a 0 (give each
+ * epoch its own log buffer to keep all of them).  policy NULL = default. */
+orloj_status orloj_replay_trace_epoch(const orloj_store *store, const orloj_latency_profile *profile,
+                                      const orloj_trace *trace, const orloj_replay_policy *policy,
+                                      const orloj_replay_epoch *epoch, orloj_counters *per_bucket,
+                                      int32_t *decision_log, void *stream);
+/* Profiler: arrival j with outcome[j] in {1, 2} (completed: "finished
+ * requests") and sample_mask[j] != 0 (sample_mask NULL = every one)
+ * adds 1 to counts[dist_id[j]][true_bin[j] - 1] — its solo execution time,
+ * which the replay knows as the hidden true bin.  counts: device uint32 [D][B],
+ * ADDED to.  Async.  Errors: INVALID_ARGUMENT, CAPACITY (D*B > 2^30), CUDA. */
+orloj_status orloj_profile_outcomes(const int32_t *dist_id, const int16_t *true_bin, const uint8_t *outcome,
+                                    const uint8_t *sample_mask, int64_t num_arrivals, uint32_t *counts,
+                                    int32_t num_dists, int32_t num_bins, void *stream);
+/* Refresh: rows d whose counts total >= max(1, min_samples) are rebuilt as
+ * orloj_store_build does (same arithmetic, bit for bit); the other rows of
+ * log2_cdf are left as they are (the previous profile stays in use until the
+ * window has enough samples; no COLD_START).  Async, no allocation. */
+orloj_status orloj_store_refresh(const uint32_t *counts, int32_t num_dists, int32_t num_bins, uint32_t min_samples,
+                                 float *log2_cdf, void *stream);
+typedef struct {
+  int32_t num_epochs;          /* E >= 1 */
+  int32_t window_epochs;       /* W >= 1: the window counts are zeroed after epochs W-1, 2W-1, ... */
+  uint32_t min_samples;        /* >= 1 */
+  const uint8_t *sample_mask;  /* device uint8 [N] or NULL: which completed requests the profiler evaluates */
+} orloj_feedback;
+size_t orloj_replay_feedback_workspace(int64_t num_scenarios, int64_t num_arrivals, int32_t num_dists,
+                                       int32_t num_bins);
+/* The whole loop, natively: for e = 0..E-1 { orloj_replay_trace_epoch(e) with
+ * the worker time carried; orloj_profile_outcomes into the window;
+ * orloj_store_refresh of `store` in place; reset the window if (e+1) % W == 0 }.
+ * store->log2_cdf is REWRITTEN (it must be writable device memory; its
+ * initial rows are the prior profile).  per_epoch_bucket: device [E][num_buckets]
+ * counters, ADDED to.  window_counts_out: device uint32 [D][B] or NULL: the
+ * window the last refresh used.  decision_logs: device int32 [E][N + S] or
+ * NULL (epoch e's log at offset e (N + S), layout as orloj_replay_trace_epoch).
+ * workspace: >= orloj_replay_feedback_workspace(S, N, D, B) bytes, 256-byte
+ * aligned.  Synchronises `stream` once at the start (reads arrival_offsets[S]);
+ * otherwise async.  Errors: as the calls it makes. */
+orloj_status orloj_replay_feedback(const orloj_store *store, const orloj_latency_profile *profile,
+                                   const orloj_trace *trace, const orloj_replay_policy *policy,
+                                   const orloj_feedback *feedback, void *workspace, size_t workspace_bytes,
+                                   orloj_counters *per_epoch_bucket, uint32_t *window_counts_out,
+                                   int32_t *decision_logs, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Eq. 1-2 priority scores and PopBatch (PAPER.md:423-455,

@@ -47,7 +47,8 @@ def _load():
         lib.oracle_cdf.argtypes = [P, i32, i32, P]
         lib.oracle_score.argtypes = [P, i32, i32, P, P, i32, i64, P, P, P, P, P, P, P, P, P, i32]
         lib.oracle_bruteforce.argtypes = [P, i32, i32, P, P, i32, P, P, i64, P, P, i32]
-        lib.oracle_replay.argtypes = [P, i32, i32, P, P, i32, i64, P, P, P, P, P, P, P, P, P, i32, i32, i32, P]
+        lib.oracle_replay.argtypes = [P, i32, i32, P, P, i32, i64, P, P, P, P, P, P, P, P, P, i32, i32, i32, P, P,
+                                      P, P]
         for f in (lib.oracle_cdf, lib.oracle_score, lib.oracle_bruteforce, lib.oracle_replay,
                   lib.oracle_max_threads):
             f.restype = ctypes.c_int32
@@ -123,12 +124,14 @@ def bruteforce(counts, a, w, deadline, dist, now, nthreads=0):
 
 
 def replay(F, a, w, arr_off, arrival, dist, true_bin, slo, follow_log=None, want_log=False, nthreads=0,
-           objective="expected_finish", drop="hopeless", counts=None):
+           objective="expected_finish", drop="hopeless", counts=None, t_start=None, want_outcome=False):
     """O2.  Returns dict(counters [S,7] int64, log | None, ties [S,3]:
     (decisions, GPU choices != oracle choice, first decision outside the tie
-    set or -1)).  objective: "expected_finish" (argmax E_k) or "finish_rate"
+    set or -1), t_end [S], outcome [N] uint8 | None (1 finished, 2 late,
+    3 dropped)).  objective: "expected_finish" (argmax E_k) or "finish_rate"
     (argmax E_k / E[L_{B_k}]); drop: "hopeless" (A16) or "expected_latency"
-    (Alg. 1, PAPER.md:351; needs `counts`)."""
+    (Alg. 1; needs `counts`).  t_start [S]: the worker is busy
+    until then (a feedback epoch continuing the previous one; None = free)."""
     F = _c(F, np.float64)
     D, B = F.shape
     a, w = _c(a, np.int64), _c(w, np.int64)
@@ -143,12 +146,15 @@ def replay(F, a, w, arr_off, arrival, dist, true_bin, slo, follow_log=None, want
     obj = {"expected_finish": 0, "finish_rate": 1}[objective]
     dm = {"hopeless": 0, "expected_latency": 1}[drop]
     cts = None if counts is None else _c(counts, np.uint32)
+    ts = None if t_start is None else _c(t_start, np.int64)
+    t_end = np.zeros(S, np.int64)
+    oc = np.zeros(N, np.uint8) if want_outcome else None
     st = _load().oracle_replay(_p(F), D, B, _p(a), _p(w), len(a), S, _p(arr_off), _p(arrival), _p(dist),
                                _p(true_bin), _p(slo), _p(counters), _p(fl), _p(log), _p(ties), nthreads, obj, dm,
-                               _p(cts))
+                               _p(cts), _p(ts), _p(t_end), _p(oc))
     if st:
         raise OracleError(f"oracle_replay status {st}")
-    return {"counters": counters, "log": log, "ties": ties}
+    return {"counters": counters, "log": log, "ties": ties, "t_end": t_end, "outcome": oc}
 
 
 def bucket_counters(counters, bucket, num_buckets):

@@ -292,7 +292,10 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
                       int32_t *log_out, int64_t *tie_info /* [S][3] or NULL */, int32_t nthreads,
                       int32_t objective /* 0: E_k, 1: E_k / E[L_{B_k}] */,
                       int32_t drop_mode /* 0: hopeless (A16), 1: expected latency (Alg. 1) */,
-                      const uint32_t *counts /* [D][B], needed for drop_mode 1 */) {
+                      const uint32_t *counts /* [D][B], needed for drop_mode 1 */,
+                      const int64_t *t_start /* [S] or NULL: worker busy until then (feedback epochs) */,
+                      int64_t *t_end /* [S] or NULL: end of the last batch */,
+                      uint8_t *outcome /* [N] or NULL: 1 finished, 2 late, 3 dropped */) {
   if (kmax < 1 || B < 1 || S < 0) return OR_EINVAL;
   if (drop_mode == 1 && !counts) return OR_EINVAL;
   set_threads(nthreads);
@@ -321,7 +324,7 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
       int64_t ndec = 0, nties = 0, first_bad = -1;
       int64_t cursor = 0;
       int32_t ncarry = 0;
-      int64_t t = INT64_MIN;
+      int64_t t = t_start ? t_start[s] : INT64_MIN;
       while (cursor < n || ncarry > 0) {
         if (ncarry == 0 && arrival[base + cursor] > t) t = arrival[base + cursor];
         /* scan: carry first, then admitted arrivals */
@@ -329,16 +332,20 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
         for (int32_t c = 0; c < ncarry; ++c) {
           int64_t r = carry[c];
           if (drop_request(F, B, a, w, arrival[base + r] + slo[s] - t, dist[base + r], drop_mode, exp_num,
-                           exp_den))
+                           exp_den)) {
             ++c_drop;
-          else win[wc++] = r;
+            if (outcome) outcome[base + r] = 3;
+          } else
+            win[wc++] = r;
         }
         while (wc < kmax && cursor < n && arrival[base + cursor] <= t) {
           int64_t r = cursor++;
           if (drop_request(F, B, a, w, arrival[base + r] + slo[s] - t, dist[base + r], drop_mode, exp_num,
-                           exp_den))
+                           exp_den)) {
             ++c_drop;
-          else win[wc++] = r;
+            if (outcome) outcome[base + r] = 3;
+          } else
+            win[wc++] = r;
         }
         ncarry = 0;
         if (wc == 0) continue;
@@ -376,8 +383,10 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
           if (true_bin[base + win[j]] > m) m = true_bin[base + win[j]];
         int64_t dur = a[k - 1] + w[k - 1] * m;
         for (int32_t j = 0; j < k; ++j) {
-          if (t + dur <= wdl[j]) ++c_fin;
+          int fin = t + dur <= wdl[j]; /* A11: inclusive deadline */
+          if (fin) ++c_fin;
           else ++c_late;
+          if (outcome) outcome[base + win[j]] = fin ? 1 : 2;
         }
         ++c_bat;
         c_busy += dur;
@@ -385,6 +394,7 @@ int32_t oracle_replay(const double *F, int32_t D, int32_t B, const int64_t *a, c
         for (int32_t j = k; j < wc; ++j) carry[ncarry++] = win[j];
       }
       if (log_out) log_out[base + s + ndec] = 0;
+      if (t_end) t_end[s] = t;
       int64_t *cs = counters + s * 7;
       cs[0] = n;
       cs[1] = c_fin;

@@ -123,13 +123,34 @@ class Profiler:
                                                          _stream_ptr(stream)))
         return self
 
+    def add_outcomes(self, trace: "Trace", outcome: torch.Tensor, sample_mask: Optional[torch.Tensor] = None,
+                     stream=None):
+        """Feedback loop: the sampled completed requests of a replay
+        (outcome 1 / 2 of orloj_replay_trace_epoch) add their solo times -- the
+        trace's hidden true bins -- to the window (orloj_profile_outcomes)."""
+        _dev(outcome, torch.uint8, "outcome")
+        if sample_mask is not None:
+            _dev(sample_mask, torch.uint8, "sample_mask")
+        D, B = self.counts.shape
+        _abi.check(_abi.lib().orloj_profile_outcomes(trace.dist.data_ptr(), trace.true_bin.data_ptr(),
+                                                     outcome.data_ptr(), _ptr(sample_mask), trace.num_arrivals,
+                                                     self.counts.data_ptr(), D, B, _stream_ptr(stream)))
+        return self
+
     def reset(self):
         self.counts.zero_()
         return self
 
-    def refresh(self, store: "HistogramStore", stream=None) -> "HistogramStore":
-        """Rebuild every row of `store` from the current window (synchronises)."""
-        return store.build_rows(self.counts, 0, stream)
+    def refresh(self, store: "HistogramStore", stream=None, min_samples: Optional[int] = None) -> "HistogramStore":
+        """Rebuild every row of `store` from the current window (orloj_store_build,
+        synchronises); with min_samples, only rows whose window holds that many
+        samples (orloj_store_refresh, async; the other rows are kept)."""
+        if min_samples is None:
+            return store.build_rows(self.counts, 0, stream)
+        D, B = self.counts.shape
+        _abi.check(_abi.lib().orloj_store_refresh(self.counts.data_ptr(), D, B, int(min_samples),
+                                                  store.log2_cdf.data_ptr(), _stream_ptr(stream)))
+        return store
 
 
 # ----------------------------------------------------------------------------
@@ -508,6 +529,71 @@ def replay_trace(store: HistogramStore, profile: LatencyProfile, trace: Trace, p
                                                  trace.num_arrivals, _ptr(workspace), workspace.numel(),
                                                  per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
     return per_bucket, log
+
+
+OUTCOME = {1: "finished", 2: "late", 3: "dropped"}
+
+
+def replay_epoch(store: HistogramStore, profile: LatencyProfile, trace: Trace, epoch: int, num_epochs: int,
+                 worker_free: Optional[torch.Tensor] = None, outcome: Optional[torch.Tensor] = None,
+                 per_bucket=None, decision_log: bool | torch.Tensor = False, stream=None):
+    """One epoch of a replay cut into num_epochs (orloj_replay_trace_epoch):
+    arrivals [floor(e n / E), floor((e+1) n / E)) of each scenario, the worker
+    busy until worker_free[s] (int64 [S], updated in place; fill with
+    INT64_MIN for a free worker), per-arrival outcomes into `outcome` (uint8
+    [N]: 1 finished, 2 late, 3 dropped).  Returns (per_bucket, log or None)."""
+    dev = trace.arrival.device
+    if per_bucket is None:
+        per_bucket = torch.zeros((trace.num_buckets, 7), dtype=torch.int64, device=dev)
+    _dev(per_bucket, torch.int64, "per_bucket")
+    if worker_free is not None:
+        _dev(worker_free, torch.int64, "worker_free")
+        if worker_free.numel() != trace.num_scenarios:
+            raise OrlojError(1, "worker_free must have one entry per scenario")
+    if outcome is not None:
+        _dev(outcome, torch.uint8, "outcome")
+        if outcome.numel() != trace.num_arrivals:
+            raise OrlojError(1, "outcome must have one entry per arrival")
+    log = None
+    if isinstance(decision_log, torch.Tensor):
+        log = _dev(decision_log, torch.int32, "decision_log")
+    elif decision_log:
+        log = torch.zeros(trace.num_arrivals + trace.num_scenarios, dtype=torch.int32, device=dev)
+    ep = _abi.ReplayEpochC(int(epoch), int(num_epochs), _ptr(worker_free), _ptr(outcome))
+    _abi.check(_abi.lib().orloj_replay_trace_epoch(store.c(), profile.c(), trace.c(), None, ctypes.byref(ep),
+                                                   per_bucket.data_ptr(), _ptr(log), _stream_ptr(stream)))
+    return per_bucket, log
+
+
+def replay_feedback(store: HistogramStore, profile: LatencyProfile, trace: Trace, num_epochs: int,
+                    window_epochs: int, min_samples: int = 1, sample_mask: Optional[torch.Tensor] = None,
+                    decision_logs: bool = False, stream=None) -> dict:
+    """The long-term feedback loop (orloj_replay_feedback):
+    epochs replayed with the current store, sampled completed requests
+    profiled, rows with >= min_samples window samples rebuilt in place in
+    `store`, the window reset every window_epochs epochs.  Returns dict(
+    per_epoch int64 [E, num_buckets, 7], window uint32-as-int32 [D, B] (the
+    window of the last refresh), logs int32 [E, N + S] or None)."""
+    dev = trace.arrival.device
+    E = int(num_epochs)
+    if sample_mask is not None:
+        _dev(sample_mask, torch.uint8, "sample_mask")
+        if sample_mask.numel() != trace.num_arrivals:
+            raise OrlojError(1, "sample_mask must have one entry per arrival")
+    per_epoch = torch.zeros((E, trace.num_buckets, 7), dtype=torch.int64, device=dev)
+    window = torch.zeros((store.num_dists, store.num_bins), dtype=torch.int32, device=dev)
+    logs = (torch.zeros((E, trace.num_arrivals + trace.num_scenarios), dtype=torch.int32, device=dev)
+            if decision_logs else None)
+    L = _abi.lib()
+    need = int(L.orloj_replay_feedback_workspace(trace.num_scenarios, trace.num_arrivals, store.num_dists,
+                                                 store.num_bins))
+    buf = torch.empty(need + 256, dtype=torch.uint8, device=dev)
+    ws = (buf.data_ptr() + 255) & ~255
+    fb = _abi.FeedbackC(E, int(window_epochs), int(min_samples), _ptr(sample_mask))
+    _abi.check(L.orloj_replay_feedback(store.c(), profile.c(), trace.c(), None, ctypes.byref(fb), ws, need,
+                                       per_epoch.data_ptr(), window.data_ptr(), _ptr(logs), _stream_ptr(stream)))
+    # the workspace is returned so it outlives the asynchronous work on `stream`
+    return {"per_epoch": per_epoch, "window": window, "logs": logs, "_workspace": buf}
 
 
 def replay_seg_stats(workspace: torch.Tensor) -> dict:

@@ -96,6 +96,16 @@ class ScoreModelC(ctypes.Structure):
                 ("num_steps", ctypes.c_int32), ("step_offset_ticks", ctypes.c_void_p), ("step_cost", ctypes.c_void_p)]
 
 
+class ReplayEpochC(ctypes.Structure):
+    _fields_ = [("epoch", ctypes.c_int32), ("num_epochs", ctypes.c_int32), ("worker_free_ticks", ctypes.c_void_p),
+                ("outcome", ctypes.c_void_p)]
+
+
+class FeedbackC(ctypes.Structure):
+    _fields_ = [("num_epochs", ctypes.c_int32), ("window_epochs", ctypes.c_int32), ("min_samples", ctypes.c_uint32),
+                ("sample_mask", ctypes.c_void_p)]
+
+
 class Counters(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("total", "finished", "dropped", "late", "batches", "busy_ticks", "span_ticks")]
@@ -135,6 +145,17 @@ SIGNATURES = {
     "orloj_pop_batch": (ctypes.c_int, [ctypes.POINTER(QueuesC), _P, ctypes.c_int32, _P, _P, _P]),
     "orloj_histogram_accumulate": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int32,
                                                   ctypes.c_int32, _P]),
+    "orloj_replay_trace_epoch": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                                ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC),
+                                                ctypes.POINTER(ReplayEpochC), _P, _P, _P]),
+    "orloj_profile_outcomes": (ctypes.c_int, [_P, _P, _P, _P, ctypes.c_int64, _P, ctypes.c_int32, ctypes.c_int32,
+                                              _P]),
+    "orloj_store_refresh": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _P, _P]),
+    "orloj_replay_feedback_workspace": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                                          ctypes.c_int32]),
+    "orloj_replay_feedback": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
+                                             ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC),
+                                             ctypes.POINTER(FeedbackC), _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "orloj_validate_store": (ctypes.c_int, [ctypes.POINTER(Store), _P]),
     "orloj_validate_queues": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC), _P]),
     "orloj_validate_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(TraceC), _P]),

@@ -21,6 +21,8 @@ bool aligned16(const void *p);
 orloj_status check_store(const orloj_store *st, int max_bins);
 orloj_status compile_profile(const orloj_latency_profile *pr, int32_t B, int kcap, ProfileDev *out);
 orloj_status check_queues(const orloj_queues *q);
+// x[0..n) = v on `stream` (async)
+cudaError_t fill_i64(int64_t *x, int64_t n, int64_t v, cudaStream_t s);
 int bins_per_lane(int B);
 int slots_for(int kmax);
 

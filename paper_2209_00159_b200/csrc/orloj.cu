@@ -103,6 +103,13 @@ orloj_status check_queues(const orloj_queues *q) {
   return ORLOJ_OK;
 }
 
+cudaError_t fill_i64(int64_t *x, int64_t n, int64_t v, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t want = (n + 255) / 256;
+  fill_i64_kernel<<<(unsigned)(want < 148 * 8 ? want : 148 * 8), 256, 0, s>>>(x, n, v);
+  return cudaGetLastError();
+}
+
 int bins_per_lane(int B) { return B <= 32 ? 1 : B <= 64 ? 2 : B <= 128 ? 4 : 8; }
 int slots_for(int kmax) {
   const int c = (kmax + 31) / 32;
@@ -477,6 +484,38 @@ orloj_status orloj_histogram_accumulate(const int32_t *dist_id, const int64_t *s
                                                                                     counts, D, B, use_smem);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "histogram_accumulate launch");
+  return ok();
+}
+
+orloj_status orloj_profile_outcomes(const int32_t *dist_id, const int16_t *true_bin, const uint8_t *outcome,
+                                    const uint8_t *sample_mask, int64_t n, uint32_t *counts, int32_t D, int32_t B,
+                                    void *stream) {
+  if (n < 0 || D < 1 || B < 1 || !counts || (n > 0 && (!dist_id || !true_bin || !outcome)))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile_outcomes: bad sizes or pointers");
+  if ((int64_t)D * B > (1ll << 30)) return fail(ORLOJ_ERR_CAPACITY, "profile_outcomes: D*B too large");
+  if (n == 0) return ok();
+  const size_t hb = (size_t)D * B * 4;
+  const int use_smem = hb <= (48u << 10);
+  const int64_t want = (n + 255) / 256;
+  const unsigned blocks = (unsigned)(want < 148 * 8 ? want : 148 * 8);
+  profile_outcomes_kernel<<<blocks, 256, use_smem ? hb : 0, (cudaStream_t)stream>>>(
+      dist_id, true_bin, outcome, sample_mask, n, counts, D, B, use_smem);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "profile_outcomes launch");
+  return ok();
+}
+
+orloj_status orloj_store_refresh(const uint32_t *counts, int32_t D, int32_t B, uint32_t min_samples, float *out,
+                                 void *stream) {
+  if (!counts || !out || D < 1 || B < 4 || B % 4)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store_refresh: need counts, out, D >= 1, B a positive multiple of 4");
+  if (B > ORLOJ_MAX_BINS) return fail(ORLOJ_ERR_CAPACITY, "store_refresh: B=%d > %d", B, ORLOJ_MAX_BINS);
+  if (!aligned16(out)) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store_refresh: out must be 16-byte aligned");
+  const int64_t threads = (int64_t)D * 32;
+  store_build_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      counts, D, B, out, nullptr, min_samples > 1 ? (uint64_t)min_samples : 1ull);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "store_refresh launch");
   return ok();
 }
 

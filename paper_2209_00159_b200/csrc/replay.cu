@@ -20,7 +20,8 @@ constexpr size_t SEG_STATS_BYTES = 256;  // workspace head: stitch statistics (i
 
 orloj_status replay_impl(const orloj_store *store, const orloj_latency_profile *profile, const orloj_trace *tr,
                          const orloj_replay_policy *policy, int32_t G, int64_t N, void *ws, size_t ws_bytes,
-                         orloj_counters *per_bucket, int32_t *log, void *stream) {
+                         orloj_counters *per_bucket, int32_t *log, void *stream,
+                         const orloj_replay_epoch *ep = nullptr) {
   orloj_status st;
   if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
   if (!policy || (policy->objective != ORLOJ_OBJ_EXPECTED_FINISH && policy->objective != ORLOJ_OBJ_FINISH_RATE &&
@@ -38,6 +39,8 @@ orloj_status replay_impl(const orloj_store *store, const orloj_latency_profile *
   if (tr->num_scenarios > 0 && (!tr->arrival_offsets || !tr->arrival_ticks || !tr->dist_id || !tr->true_bin ||
                                 !tr->slo_ticks || !tr->bucket || !per_bucket))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "trace arrays / per_bucket must be non-NULL device pointers");
+  if (ep && (ep->num_epochs < 1 || ep->epoch < 0 || ep->epoch >= ep->num_epochs))
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay epoch: need 0 <= epoch < num_epochs");
   if (G < 1 || G > ORLOJ_REPLAY_MAX_SEGMENTS)
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay: segments=%d outside 1..%d", G, ORLOJ_REPLAY_MAX_SEGMENTS);
   if (G > 1) {
@@ -74,6 +77,13 @@ orloj_status replay_impl(const orloj_store *store, const orloj_latency_profile *
   p.counters = reinterpret_cast<unsigned long long *>(per_bucket);
   p.log = log;
   p.drop_thr = policy->drop_threshold_ticks;
+  p.num_epochs = 1;
+  if (ep) {
+    p.epoch = ep->epoch;
+    p.num_epochs = ep->num_epochs;
+    p.t_carry = ep->worker_free_ticks;
+    p.outcome = ep->outcome;
+  }
   if (alg1) {
     p.size_thr = policy->size_threshold_ticks;
     p.prio_table = policy->priority_table;
@@ -138,6 +148,82 @@ orloj_status orloj_replay_trace_seg(const orloj_store *store, const orloj_latenc
   const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
   return replay_impl(store, profile, tr, policy ? policy : &def, segments, num_arrivals, workspace, workspace_bytes, per_bucket,
                      log, stream);
+}
+
+orloj_status orloj_replay_trace_epoch(const orloj_store *store, const orloj_latency_profile *profile,
+                                      const orloj_trace *tr, const orloj_replay_policy *policy,
+                                      const orloj_replay_epoch *epoch, orloj_counters *per_bucket, int32_t *log,
+                                      void *stream) {
+  const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
+  if (!epoch) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_trace_epoch: epoch descriptor is NULL");
+  return replay_impl(store, profile, tr, policy ? policy : &def, 1, 0, nullptr, 0, per_bucket, log, stream, epoch);
+}
+
+size_t orloj_replay_feedback_workspace(int64_t num_scenarios, int64_t num_arrivals, int32_t num_dists,
+                                       int32_t num_bins) {
+  if (num_scenarios < 0 || num_arrivals < 0 || num_dists < 1 || num_bins < 1) return 0;
+  return align256((size_t)num_scenarios * 8) + align256((size_t)num_arrivals) +
+         align256((size_t)num_dists * num_bins * 4);
+}
+
+orloj_status orloj_replay_feedback(const orloj_store *store, const orloj_latency_profile *profile,
+                                   const orloj_trace *tr, const orloj_replay_policy *policy,
+                                   const orloj_feedback *fb, void *workspace, size_t workspace_bytes,
+                                   orloj_counters *per_epoch_bucket, uint32_t *window_counts_out,
+                                   int32_t *decision_logs, void *stream) {
+  orloj_status st;
+  if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
+  if (!fb || fb->num_epochs < 1 || fb->window_epochs < 1 || fb->min_samples < 1)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_feedback: need num_epochs >= 1, window_epochs >= 1, "
+                "min_samples >= 1");
+  if (!tr || !per_epoch_bucket)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_feedback: trace / per_epoch_bucket NULL");
+  const int64_t S = tr->num_scenarios;
+  const int32_t D = store->num_dists, B = store->num_bins;
+  if (S < 0) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_feedback: num_scenarios < 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  // the arrival count sizes the outcome buffer: read arrival_offsets[S] (synchronous; off the hot path)
+  int64_t N = 0;
+  if (S > 0) {
+    if (!tr->arrival_offsets) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_feedback: arrival_offsets NULL");
+    cudaError_t e = cudaMemcpyAsync(&N, tr->arrival_offsets + S, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "replay_feedback: reading arrival_offsets[S]");
+  }
+  const size_t need = orloj_replay_feedback_workspace(S, N, D, B);
+  if (!workspace || ((uintptr_t)workspace & 255u) || workspace_bytes < need)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_feedback: need a 256-byte aligned device workspace of %zu "
+                "bytes (got %zu)", need, workspace_bytes);
+  char *w = reinterpret_cast<char *>(workspace);
+  int64_t *t_carry = reinterpret_cast<int64_t *>(w);
+  uint8_t *outcome = reinterpret_cast<uint8_t *>(w + align256((size_t)S * 8));
+  uint32_t *counts = reinterpret_cast<uint32_t *>(w + align256((size_t)S * 8) + align256((size_t)N));
+  cudaError_t e = fill_i64(t_carry, S, INT64_MIN, s);  // the worker starts free
+  if (e == cudaSuccess) e = cudaMemsetAsync(counts, 0, (size_t)D * B * 4, s);
+  if (e != cudaSuccess) return cuda_fail(e, "replay_feedback: memset");
+  float *rows = const_cast<float *>(store->log2_cdf);  // rewritten in place at every refresh (header)
+  for (int32_t ep = 0; ep < fb->num_epochs; ++ep) {
+    // (1) replay epoch ep with the current store (static during the epoch, A18)
+    if (N > 0 && (e = cudaMemsetAsync(outcome, 0, (size_t)N, s)) != cudaSuccess)
+      return cuda_fail(e, "replay_feedback: memset");
+    const orloj_replay_epoch rep{ep, fb->num_epochs, t_carry, outcome};
+    st = orloj_replay_trace_epoch(store, profile, tr, policy, &rep, per_epoch_bucket + (int64_t)ep * tr->num_buckets,
+                                  decision_logs ? decision_logs + (int64_t)ep * (N + S) : nullptr, stream);
+    if (st) return st;
+    // (2) the profiler evaluates the sampled completed requests solo
+    if ((st = orloj_profile_outcomes(tr->dist_id, tr->true_bin, outcome, fb->sample_mask, N, counts, D, B, stream)))
+      return st;
+    // (3) the scheduler picks the window up: rows with enough samples are rebuilt
+    if ((st = orloj_store_refresh(counts, D, B, fb->min_samples, rows, stream))) return st;
+    // (4) the profiling memory is reset every window_epochs epochs
+    if (window_counts_out && ep == fb->num_epochs - 1 &&
+        (e = cudaMemcpyAsync(window_counts_out, counts, (size_t)D * B * 4, cudaMemcpyDeviceToDevice, s)) !=
+            cudaSuccess)
+      return cuda_fail(e, "replay_feedback: copy of the window counts");
+    if ((ep + 1) % fb->window_epochs == 0 && (e = cudaMemsetAsync(counts, 0, (size_t)D * B * 4, s)) != cudaSuccess)
+      return cuda_fail(e, "replay_feedback: window reset");
+  }
+  return ok();
 }
 
 }  // extern "C"

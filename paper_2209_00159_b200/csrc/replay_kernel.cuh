@@ -76,6 +76,12 @@ struct ReplayParams {
   unsigned long long *seg_stats;  // [5]: decisions re-run by the stitch, segments joined, segments crossed,
                                   //      decisions in the extensions, inconsistent-size flag (zeroed by the host)
   int64_t num_arrivals;           // MODE 1 / 2: the caller's arrival_offsets[S] (sizes seg_log)
+  // MODE 0 epochs (feedback loop, include/orloj.h orloj_replay_epoch): replay only
+  // arrivals [s_e, s_{e+1}) of each scenario, the worker free at t_carry[s]
+  // (written back at the end), per-arrival outcomes (1 finished, 2 late, 3 dropped)
+  int32_t epoch, num_epochs;
+  int64_t *t_carry;
+  uint8_t *outcome;
 };
 
 constexpr int SEG_REC = 20;  // regeneration points recorded per list
@@ -134,7 +140,7 @@ template <int BPL, bool RATE = false>
 struct ReplayWarpSmem {
   static constexpr int STG = 32 * BPL + 4;
   static constexpr int PSTRIDE = 36;
-  static constexpr size_t BYTES = (size_t)(REPLAY_KB * STG) * 4 + 32 * (8 + 8 + 4 + 4) +
+  static constexpr size_t BYTES = (size_t)(REPLAY_KB * STG) * 4 + 32 * (8 + 8 + 4 + 4 + 4) +
                                   (RATE ? 2 : 1) * 32 * PSTRIDE * 4 + 16;  // + segment-run state (MODE 1)
   __host__ __device__ static constexpr size_t bytes() { return BYTES; }
 };
@@ -169,7 +175,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int64_t *w_h = w_dl + 32;                                                 // window hopeless times
   int32_t *w_d = reinterpret_cast<int32_t *>(w_h + 32);                     // window distributions
   int32_t *w_tb = w_d + 32;                                                 // window true bins
-  float *Pm = reinterpret_cast<float *>(w_tb + 32);                         // P[k-1][r], stride PST
+  int32_t *w_ix = w_tb + 32;  // window arrival indices (MODE 0 with per-arrival outcomes only)
+  float *Pm = reinterpret_cast<float *>(w_ix + 32);                         // P[k-1][r], stride PST
   float *Sm = Pm + 32 * PST;  // RATE only: per-lane partial sum_{i<B} G_k(tau_i), [k-1][lane]
   // MODE 1 (cold, warp-uniform; kept out of registers): base arrival of the
   // current record list, records in it, extension flag
@@ -210,8 +217,17 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   }
 
   const int kmax = p.prof.kmax;
-  const int64_t base = p.arr_off[s];
-  const int64_t n = p.arr_off[s + 1] - base;
+  int64_t base = p.arr_off[s];
+  int64_t n = p.arr_off[s + 1] - base;
+  uint8_t *oc = nullptr;  // MODE 0: per-arrival outcomes (indexed like arr / dis / tbs)
+  if constexpr (MODE == 0) {
+    if (p.num_epochs > 1) {  // epoch e: arrivals [s_e, s_{e+1}) of the scenario
+      const int64_t b0 = seg_begin(n, p.epoch, p.num_epochs);
+      base += b0;
+      n = seg_begin(n, p.epoch + 1, p.num_epochs) - b0;
+    }
+    if (p.outcome) oc = p.outcome + base;
+  }
   const int64_t slo = p.slo[s];
   const int64_t *arr = p.arrival + base;
   const int32_t *dis = p.dist + base;
@@ -228,6 +244,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int32_t my_ak = (ALG1 && lane < kmax) ? p.prof.a[lane] : 0;
 
   int64_t t = INT64_MIN;
+  if constexpr (MODE == 0)
+    if (p.t_carry) t = p.t_carry[s];  // the worker is busy until then (INT64_MIN: free)
   int64_t cursor = 0;
   int64_t seg_end = INT64_MAX;  // MODE 1: stop (s_{g+1}, then the extension cap); MODE 2: s_{g+1} of the stitched g
   int64_t rec_at = INT64_MAX;  // MODE 1: record the first regeneration point at or past this arrival
@@ -495,6 +513,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         const bool ok = lane < 31 && va && an > tpj && tpj <= hj;
         const int m = __ffs(~__ballot_sync(FULL, ok)) - 1;  // >= 1 (lane 0 passed ok0)
         const unsigned fm = __ballot_sync(FULL, lane < m && Tj <= ua + slo);
+        if (oc && lane < m) oc[cursor + lane] = ((fm >> lane) & 1u) ? 1 : 2;
         c_fin += __popc(fm);
         c_late += m - __popc(fm);
         c_bat += m;
@@ -513,17 +532,19 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     if (ncarry > 0) {
       const bool valid = lane < ncarry;
       int64_t Dr = 0, hr = 0;
-      int dr = 0, tr = 0;
+      int dr = 0, tr = 0, ir = 0;
       if (valid) {
         Dr = w_dl[carry_off + lane];
         hr = w_h[carry_off + lane];
         dr = w_d[carry_off + lane];
         tr = w_tb[carry_off + lane];
+        if (oc) ir = w_ix[carry_off + lane];
       }
       const bool keep = valid && t <= hr;
       const unsigned vm = __ballot_sync(FULL, valid);
       const unsigned km = __ballot_sync(FULL, keep);
       c_drop += __popc(vm & ~km);
+      if (oc && valid && !keep) oc[ir] = 3;
       __syncwarp();
       if (keep) {
         const int slot = __popc(km & ((1u << lane) - 1u));
@@ -531,6 +552,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         w_h[slot] = hr;
         w_d[slot] = dr;
         w_tb[slot] = tr;
+        if (oc) w_ix[slot] = ir;
       }
       wc = __popc(km);
     }
@@ -552,12 +574,14 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       }
       const unsigned kc = km & consumed;
       c_drop += __popc(vm & consumed & ~km);
+      if (oc && ((vm & consumed & ~km) >> lane) & 1u) oc[cursor + lane] = 3;
       if ((kc >> lane) & 1u) {
         const int slot = wc + __popc(kc & ((1u << lane) - 1u));
         w_dl[slot] = ua + slo;
         w_h[slot] = uh;
         w_d[slot] = ud;
         w_tb[slot] = ut;
+        if (oc) w_ix[slot] = (int32_t)(cursor + lane);
       }
       wc += __popc(kc);
       const int nc = __popc(consumed);
@@ -702,6 +726,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
                                    (int64_t)__shfl_sync(FULL, my_wk, kstar - 1) * mbin
                              : (int64_t)p.prof.a[kstar - 1] + (int64_t)p.prof.w[kstar - 1] * mbin;
     const unsigned fm = __ballot_sync(FULL, sel && t + dur <= Dr);
+    const int ix = (oc && mem) ? w_ix[lane] : 0;
+    if (oc && sel) oc[ix] = ((fm >> lane) & 1u) ? 1 : 2;
     c_fin += __popc(fm);
     c_late += kstar - __popc(fm);
     c_bat += 1;
@@ -722,6 +748,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         w_h[slot] = hr;
         w_d[slot] = dr;
         w_tb[slot] = tb;
+        if (oc) w_ix[slot] = ix;
       }
       carry_off = 0;
     }
@@ -746,6 +773,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   }
   if (lane == 0) {
     if (mylog) mylog[ndec] = 0;
+    if constexpr (MODE == 0)
+      if (p.t_carry) p.t_carry[s] = t;
     unsigned long long *cs = p.counters + (int64_t)p.bucket[s] * 7;
     atomicAdd(cs + 0, (unsigned long long)n);
     atomicAdd(cs + 1, (unsigned long long)c_fin);

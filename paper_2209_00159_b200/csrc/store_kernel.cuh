@@ -9,8 +9,12 @@
 
 namespace orloj {
 
+// min_total: rows with fewer samples are left as they are (the feedback loop's
+// refresh keeps a row until its window holds enough samples); a row with total
+// 0 sets *cold when `cold` is given (orloj_store_build: COLD_START).
 __global__ void store_build_kernel(const uint32_t *__restrict__ counts, int32_t D, int32_t B,
-                                   float *__restrict__ out, unsigned int *__restrict__ cold) {
+                                   float *__restrict__ out, unsigned int *__restrict__ cold,
+                                   uint64_t min_total = 1) {
   const int lane = threadIdx.x & 31;
   const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (d >= D) return;
@@ -19,8 +23,8 @@ __global__ void store_build_kernel(const uint32_t *__restrict__ counts, int32_t 
   for (int i = lane; i < B; i += 32) total += row[i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(FULL, total, o);
-  if (total == 0) {
-    if (lane == 0) atomicOr(cold, 1u);
+  if (total == 0 || total < min_total) {
+    if (total == 0 && cold && lane == 0) atomicOr(cold, 1u);
     return;
   }
   uint64_t carry = 0;
@@ -72,6 +76,42 @@ __global__ void hist_accumulate_kernel(const int32_t *__restrict__ dist, const i
     for (int e = threadIdx.x; e < DB; e += blockDim.x)
       if (s_h[e]) atomicAdd(&counts[e], s_h[e]);
   }
+}
+
+// Long-term feedback loop ("finished requests are sampled
+// and sent to the profiler to evaluate individually"): a replayed arrival whose
+// outcome is completed (1 finished, 2 late; 3 = dropped never ran) and whose
+// sample mask is non-zero adds its solo execution time — in the replay the
+// hidden true bin — to counts[d][bin-1].  Same CTA-private histogram scheme.
+__global__ void profile_outcomes_kernel(const int32_t *__restrict__ dist, const int16_t *__restrict__ true_bin,
+                                        const uint8_t *__restrict__ outcome, const uint8_t *__restrict__ mask,
+                                        int64_t n, uint32_t *__restrict__ counts, int32_t D, int32_t B,
+                                        int use_smem) {
+  extern __shared__ uint32_t s_h[];
+  const int DB = D * B;
+  if (use_smem) {
+    for (int e = threadIdx.x; e < DB; e += blockDim.x) s_h[e] = 0;
+    __syncthreads();
+  }
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned oc = outcome[j];
+    if ((oc != 1u && oc != 2u) || (mask && !mask[j])) continue;
+    const int d = dist[j], i = true_bin[j];
+    if (d < 0 || d >= D || i < 1 || i > B) continue;
+    const int e = d * B + i - 1;
+    if (use_smem) atomicAdd(&s_h[e], 1u);
+    else atomicAdd(&counts[e], 1u);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < DB; e += blockDim.x)
+      if (s_h[e]) atomicAdd(&counts[e], s_h[e]);
+  }
+}
+
+__global__ void fill_i64_kernel(int64_t *__restrict__ x, int64_t n, int64_t v) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    x[j] = v;
 }
 
 // flags: bit0 = value / shape violation, bit1 = order violation

@@ -152,3 +152,29 @@ def test_segmented_other_bin_widths(B):
         pb0, log0, pb1, log1, pb2 = _both(store, prof, tr, G)
         assert (pb1 == pb0).all() and (pb2 == pb0).all() and (log1 == log0).all(), G
     assert pb0[:, 4].sum() > S  # scenarios actually batched
+
+
+def test_size_guard_flags_short_num_arrivals():
+    """The segmented replay sizes its scratch logs from the caller's
+    num_arrivals: a value below arrival_offsets[S] must not write out of
+    bounds -- the call does nothing and sets the size-error diagnostic."""
+    import ctypes
+    from paper_2209_00159_b200 import _abi
+    tf, off, arr, dist, tb, slo = _family("gpt", 1, 3000)
+    store = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks)
+    prof = orj.LatencyProfile(tf.profile.a, tf.profile.w)
+    tr = _trace(off, arr, dist, tb, slo)
+    G, short = 4, len(arr) // 2
+    need = orj.replay_seg_workspace_bytes(tr, G, True)
+    ws = torch.zeros(need + 4096, dtype=torch.uint8, device="cuda")
+    pb = torch.zeros((tr.num_buckets, 7), dtype=torch.int64, device="cuda")
+    log = torch.zeros(len(arr) + len(slo), dtype=torch.int32, device="cuda")
+    pol = _abi.ReplayPolicyC(0, None, None, None, None, 0.0)
+    need_short = _abi.lib().orloj_replay_seg_workspace(tr.num_scenarios, short, G, 1)
+    st = _abi.lib().orloj_replay_trace_seg(store.c(), prof.c(), tr.c(), ctypes.byref(pol), G, short, ws.data_ptr(),
+                                           need_short, pb.data_ptr(), log.data_ptr(), None)
+    assert st == 0
+    torch.cuda.synchronize()
+    assert orj.replay_seg_stats(ws)["size_error"] == 1
+    assert int(pb.abs().sum()) == 0 and int(log.abs().sum()) == 0
+    assert int(ws[need_short:].abs().sum()) == 0          # nothing written past the declared workspace
