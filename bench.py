@@ -910,6 +910,106 @@ def run_policies(args, rank, world, dev):
     return out
 
 
+B_SWEEP_PER_MS = (1e-6, 1e-5, 1e-4, 1e-3, 1e-2, 1e-1)
+
+
+def run_b_sweep(args, rank, world, dev):
+    """Alg. 1 replay finish rate per SLO bucket as the anticipated-delay rate b
+    of the Eq. 1-2 priority varies over 1e-6 .. 1e-1 per ms (PAPER.md:886-902,
+    fig. eval-lambdas; the paper reports insensitivity, :623): the policy-sweep
+    scenarios (32 seeds per bucket), segmented replay, counters summed over
+    ranks.  The Eq. 2 tables are rebuilt per b (off the critical path)."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    from paper_2209_00159_b200 import parallel, policy
+
+    a2 = argparse.Namespace(**vars(args))
+    a2.replay_seeds = args.policy_seeds
+    fams = build_replay(a2, rank, world, dev)
+    nb = len(gen.BUCKET_SLO_MULTS)
+    segs = [replay_segments(args.replay_segments, f.trace.num_scenarios, args.replay_arrivals) for f in fams]
+    wss = [torch.empty(max(orj.replay_seg_workspace_bytes(f.trace, g), 1), dtype=torch.uint8, device=dev)
+           for f, g in zip(fams, segs)]
+    thr = [torch.from_numpy(policy.alg1_size_thresholds(f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).to(dev)
+           for f in fams]
+    out = {"sweep": f"4 families x 8 buckets x {args.policy_seeds} seeds x {args.replay_arrivals} arrivals, "
+                    "Alg. 1 (Eq. 1-2 PopBatch)", "b_per_ms": list(B_SWEEP_PER_MS), "finish_rate_by_bucket": {},
+           "ms": []}
+    for b_ms in B_SWEEP_PER_MS:
+        b = b_ms / 1000.0                     # 1 tick = 1 us
+        tabs = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
+        pts = [orj.PriorityTable(f.store, f.profile, f.profile.kmax, b) for f in fams]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for f, t_, pt, st, g, ws in zip(fams, tabs, pts, thr, segs, wss):
+            orj.replay_trace(f.store, f.profile, f.trace, per_bucket=t_, objective="alg1", priority=pt,
+                             size_thresholds=st, segments=g, workspace=ws)
+        e1.record()
+        parallel.allreduce_counters(tabs)
+        torch.cuda.synchronize()
+        c = tabs.cpu().numpy()
+        out["ms"].append(round(e0.elapsed_time(e1), 3))
+        out["finish_rate_by_bucket"][f"{b_ms:g}"] = {
+            f.tf.fam.name: [round(float(x), 4) for x in c[i, :, 1] / np.maximum(c[i, :, 0], 1)]
+            for i, f in enumerate(fams)}
+    rates = np.array([[v for fam in d.values() for v in fam] for d in out["finish_rate_by_bucket"].values()])
+    out["max_spread_over_b"] = round(float((rates.max(0) - rates.min(0)).max()), 4)
+    return out
+
+
+FEEDBACK_EPOCHS, FEEDBACK_WINDOW, FEEDBACK_MIN, FEEDBACK_SAMPLE = 8, 2, 200, 0.125
+
+
+def run_feedback(args, rank, world, dev):
+    """Long-term feedback loop: the
+    policy-sweep scenarios with an input drift half-way (half the
+    applications 1.5x slower from epoch 4 of 8), replayed epoch by epoch
+    (orloj_replay_feedback: profiler of 1/8 of the completed requests,
+    refresh of rows with >= 200 window samples, window reset every 2
+    epochs) against the same epochs with the static pre-drift store (no
+    refresh).  Finish rate per epoch, all buckets pooled."""
+    import torch
+
+    import gen
+    import paper_2209_00159_b200 as orj
+    import workloads as wl
+    from paper_2209_00159_b200 import parallel
+
+    nb = len(gen.BUCKET_SLO_MULTS)
+    u = np.arange(nb * args.policy_seeds)
+    mine = parallel.shard_round_robin(u // nb, rank, world)
+    E = FEEDBACK_EPOCHS
+    res = {"workload": f"4 families x 8 buckets x {args.policy_seeds} seeds x {args.replay_arrivals} arrivals; "
+                       f"drift at epoch {E // 2} of {E}", "epochs": E, "window_epochs": FEEDBACK_WINDOW,
+           "min_samples": FEEDBACK_MIN, "sample_rate": FEEDBACK_SAMPLE, "finish_rate_by_epoch": {}, "ms": {}}
+    for name in gen.C5_FAMILIES:
+        if name == "static":
+            continue                  # point masses: the drift only relabels the single bin
+        f = wl.C5Family(name, local_ids=mine, n_arr=args.replay_arrivals, seeds_per_bucket=args.policy_seeds,
+                        device=dev, drift=(E, E // 2))
+        mask = wl.t(gen.sample_mask(gen.SEED_BASE + 41, f.trace.num_arrivals, FEEDBACK_SAMPLE), np.uint8, dev)
+        rates = {}
+        for mode, m in (("static", 1 << 31), ("feedback", FEEDBACK_MIN)):
+            st = orj.HistogramStore.from_counts(f.tf.fam.counts, f.tf.fam.bin_ticks, dev)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = orj.replay_feedback(st, f.profile, f.trace, E, FEEDBACK_WINDOW, m, sample_mask=mask)
+            e1.record()
+            pe = r["per_epoch"]
+            parallel.allreduce_counters(pe.view(-1, 7))
+            torch.cuda.synchronize()
+            c = pe.cpu().numpy().sum(1)            # [E][7], buckets pooled
+            rates[mode] = [round(float(x), 4) for x in c[:, 1] / np.maximum(c[:, 0], 1)]
+            res["ms"][f"{name}/{mode}"] = round(e0.elapsed_time(e1), 3)
+        res["finish_rate_by_epoch"][name] = rates
+        del f
+    return res
+
+
 def run_replay(args, rank, world, dev, barrier, max_over_ranks):
     import gen
 
@@ -949,6 +1049,8 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
                            "peak_source": "148 SMs x 4 warp schedulers x 1 instruction/cycle at sm_max_mhz"}
     if not args.no_policies:
         out["policies"] = run_policies(args, rank, world, dev)
+        out["b_sweep"] = run_b_sweep(args, rank, world, dev)
+        out["feedback"] = run_feedback(args, rank, world, dev)
     if world == 1 and not args.no_shard_proxy:
         # strong-scaling proxy on one GPU: time EVERY rank's shard of an N-GPU run
         # (median of 3 sweeps each; everything but the ~10 us all-reduce) and take

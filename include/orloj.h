@@ -258,6 +258,32 @@ orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency
                                    const orloj_trace *trace, const orloj_replay_policy *policy,
                                    orloj_counters *per_bucket, int32_t *decision_log, void *stream);
 
+/* Exact thresholds for the replay policies (host arrays; synchronous host
+ * computation, no device work; off the critical path like the paper's per-bs
+ * precompute).  counts: host uint32 [D][B], every row with a
+ * positive total (COLD_START otherwise).  Both are exact ceilings of exact
+ * rationals (no floating point):
+ *  - orloj_expected_latency_thresholds: thr[d] = a_1 + ceil(w_1 sum_i i c_{d,i} /
+ *    sum_i c_{d,i}) — EstimateBatchLatency(r, 1) of Alg. 1's drop under
+ *    the E_k scorer's model (A1: a batch of one whose member sits in bin m runs
+ *    a_1 + w_1 m), the drop_threshold_ticks of ORLOJ_OBJ_EXPECTED_FINISH /
+ *    FINISH_RATE replays.  thr: host int64 [D].
+ *  - orloj_alg1_size_thresholds: thr_bs = ceil(E[L_bs]) for bs = 1..kmax under
+ *    Alg. 1's batch model (R10/R11: bs i.i.d. draws from the weighted mixture
+ *    of all applications, each bin's mass uniform within it as in Eq. 2):
+ *    E[L_bs] = a_bs + w_bs sum_i (G_i - G_{i-1}) (i - 1/2), G_i = F_mix(tau_i)^bs —
+ *    the size_threshold_ticks of ORLOJ_OBJ_ALG1.  weights: host double [D] (>= 0,
+ *    not all 0; each taken as the exact dyadic rational it is) or NULL
+ *    (uniform).  thr: host int64 [kmax].  CAPACITY if the common denominator
+ *    of the mixture exceeds 2^65536.
+ * The two readings of a bin's mass (upper edge vs uniform) differ on purpose:
+ * each threshold belongs to the model its policy scores with. */
+orloj_status orloj_expected_latency_thresholds(const uint32_t *counts, int32_t num_dists, int32_t num_bins,
+                                               const orloj_latency_profile *profile, int64_t *thr);
+orloj_status orloj_alg1_size_thresholds(const uint32_t *counts, int32_t num_dists, int32_t num_bins,
+                                        const double *weights, const orloj_latency_profile *profile,
+                                        int64_t *thr);
+
 /* Segmented replay: the same replay (every counter and decision-log entry
  * identical to orloj_replay_trace_ex, bit for bit) with a shorter critical
  * path.  Each scenario's arrivals are cut into `segments` equal ranges

@@ -156,6 +156,10 @@ SIGNATURES = {
     "orloj_replay_feedback": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile),
                                              ctypes.POINTER(TraceC), ctypes.POINTER(ReplayPolicyC),
                                              ctypes.POINTER(FeedbackC), _P, ctypes.c_size_t, _P, _P, _P, _P]),
+    "orloj_expected_latency_thresholds": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32,
+                                                         ctypes.POINTER(LatencyProfile), _P]),
+    "orloj_alg1_size_thresholds": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, _P,
+                                                  ctypes.POINTER(LatencyProfile), _P]),
     "orloj_validate_store": (ctypes.c_int, [ctypes.POINTER(Store), _P]),
     "orloj_validate_queues": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC), _P]),
     "orloj_validate_trace": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(TraceC), _P]),

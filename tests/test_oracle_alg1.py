@@ -128,3 +128,48 @@ def test_replay_invariants_and_follow_own_log():
         bad[idx[0]] = 0b101
         assert alg1.replay(tf.fam.counts, tf.profile.a, tf.profile.w, b, off, arr, dist, tb, slo, thr,
                            follow_log=bad)["ties"][:, 2].max() >= 0
+
+
+def test_abi_thresholds_equal_exact_rationals():
+    """orloj_alg1_size_thresholds (C ABI, big-integer arithmetic) equals the
+    oracle's exact-rational evaluation on random histograms with empty bins,
+    unequal totals, zero and non-dyadic weights, point masses, kmax 32; and
+    orloj_expected_latency_thresholds equals ceil of the exact rational
+    a_1 + w_1 sum_i i c_i / sum_i c_i."""
+    from fractions import Fraction
+    rng = np.random.default_rng(gen.SEED_BASE + 931)
+    for trial in range(12):
+        D = int(rng.integers(1, 9))
+        B = int(rng.choice([4, 8, 16, 64]))
+        counts = rng.integers(0, 1 << int(rng.integers(3, 31)), size=(D, B)).astype(np.uint32)
+        counts[rng.random((D, B)) < 0.4] = 0
+        counts[:, int(rng.integers(0, B))] += 1
+        if trial % 4 == 0:
+            counts[0] = 0
+            counts[0, B // 2] = 5                        # a point mass
+        a = np.cumsum(rng.integers(0, 3000, 32)).astype(np.int64)
+        w = np.cumsum(rng.integers(0, 500, 32)).astype(np.int64) + 1
+        wts = None if trial % 3 == 0 else rng.random(D) * 3
+        if wts is not None and D > 1:
+            wts[0] = 0.0
+        ref = alg1.size_thresholds(counts, a, w, wts)
+        got = policy.alg1_size_thresholds(counts, a, w, wts)
+        assert np.array_equal(got, ref), trial
+        el = policy.expected_latency_thresholds(counts, a, w)
+        for d in range(D):
+            e = Fraction(int(a[0])) + Fraction(int(w[0]) * sum((i + 1) * int(c) for i, c in enumerate(counts[d])),
+                                                int(counts[d].sum()))
+            assert el[d] == math.ceil(e)
+
+
+def test_abi_thresholds_errors():
+    import pytest
+    from paper_2209_00159_b200 import OrlojError
+    counts = np.ones((2, 8), np.uint32)
+    counts[1] = 0
+    with pytest.raises(OrlojError, match="COLD_START"):
+        policy.alg1_size_thresholds(counts, [0], [1])
+    with pytest.raises(OrlojError, match="COLD_START"):
+        policy.expected_latency_thresholds(counts, [0], [1])
+    with pytest.raises(OrlojError, match="INVALID"):
+        policy.alg1_size_thresholds(np.ones((2, 8)), [0], [1], weights=[0.0, 0.0])

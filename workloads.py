@@ -55,7 +55,9 @@ class C5Family:
     """One family of the C5 sweep on the device: store, profile, trace."""
 
     def __init__(self, name: str, local_ids=None, n_arr: int = gen.C5_ARRIVALS,
-                 seeds_per_bucket: int = gen.C5_SEEDS_PER_BUCKET, device="cuda", on_host=False):
+                 seeds_per_bucket: int = gen.C5_SEEDS_PER_BUCKET, device="cuda", on_host=False, drift=None):
+        """drift = (num_epochs, drift_epoch): true bins from epoch drift_epoch on
+        come from gen.drifted_trace_family (feedback-loop workload)."""
         self.tf = gen.c5_trace_family(name)
         gids, bucket, slo = gen.c5_scenarios(self.tf, seeds_per_bucket)
         if local_ids is not None:
@@ -82,6 +84,21 @@ class C5Family:
                                              arrival.data_ptr(), dist_t.data_ptr(), tb_t.data_ptr(),
                                              torch.cuda.current_stream().cuda_stream)
             assert st == 0, f"gen_trace_dev failed ({st})"
+            if drift is not None:
+                E, e0 = drift
+                self.tfd = gen.drifted_trace_family(self.tf)
+                cum2 = t(self.tfd.cum.view(np.int32), np.int32, device)
+                a2 = torch.empty_like(arrival)
+                d2 = torch.empty_like(dist_t)
+                tb2 = torch.empty_like(tb_t)
+                st = gen.dev_lib().gen_trace_dev(self.tf.seed, g.data_ptr(), S, n_arr, e.data_ptr(),
+                                                 self.tf.base_gap, self.tf.fam.D, cum2.data_ptr(), self.tf.fam.B,
+                                                 gen.T0, a2.data_ptr(), d2.data_ptr(), tb2.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream)
+                assert st == 0, f"gen_trace_dev failed ({st})"
+                j0 = (e0 * n_arr) // E
+                tb_t.view(S, n_arr)[:, j0:] = tb2.view(S, n_arr)[:, j0:]
+                del a2, d2, tb2
         self.trace = orj.Trace(t(self.offsets_np, np.int64, device), arrival, dist_t, tb_t,
                                t(slo, np.int64, device), t(bucket, np.int32, device), len(gen.BUCKET_SLO_MULTS))
 
