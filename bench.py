@@ -791,7 +791,31 @@ def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
     return int(max(1, min(g, n_arr // 2000, 4096)))
 
 
-REPLAY_SWEEP_WARP_INSTR = 87_906_266_861  # ncu, full C5 sweep at 8 segments (profiles/r01_replay_sweep_n1_launches.csv)
+REPLAY_LAUNCHES = os.path.join(ROOT, "profiles", "replay_sweep_launches.csv")
+
+
+def replay_sweep_instructions():
+    """Warp instructions of one full 1-GPU C5 sweep at 8 segments: the sum of
+    smsp__inst_executed.sum over the last sweep's launches in the committed
+    ncu launch list (profiles/replay_sweep_launches.csv, re-captured with
+    scripts/gpu_replay_check.sh whenever the replay kernel changes).  The
+    count is a property of the deterministic workload and the code."""
+    import csv
+    if not os.path.exists(REPLAY_LAUNCHES):
+        return None
+    with open(REPLAY_LAUNCHES) as f:
+        lines = [l for l in f if l.startswith('"')]
+    rows = list(csv.reader(lines))
+    h = rows[0]
+    iI, iM, iV = h.index("ID"), h.index("Metric Name"), h.index("Metric Value")
+    per = {}
+    for r in rows[1:]:
+        if r[iM] == "smsp__inst_executed.sum":
+            per[int(r[iI])] = float(r[iV].replace(",", ""))
+    ids = sorted(per)
+    if len(ids) < 8:
+        return None
+    return int(sum(per[i] for i in ids[-8:]))      # one sweep = 4 families x 2 launches
 
 
 def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True, segments="auto"):
@@ -1036,16 +1060,18 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
            "gpu_launches_per_sweep": sum(2 if g > 1 else 1 for g in segs), "clocks": clk,
            "collective": "one torch.distributed.all_reduce of the int64 [4 x 8 x 7] counters (NCCL) per sweep, "
                          "inside the timed region"}
+    instr = replay_sweep_instructions()
     if (world == 1 and segs == [8, 8, 8, 8] and args.replay_seeds == 256
-            and args.replay_arrivals == 100_000):
+            and args.replay_arrivals == 100_000 and instr):
         # issue roofline of the full 1-GPU sweep: the warp-instruction count is a
-        # property of the (deterministic) workload, counted once by ncu
-        # (profiles/r01_replay_sweep_n1_launches.csv: smsp__inst_executed.sum of
-        # the 8 launches of one sweep); the time is this run's
+        # property of the (deterministic) workload and the code, counted by ncu
+        # on the committed code (profiles/replay_sweep_launches.csv); the time is this run's
         peak = 148 * 4 * clk.get("sm_max_mhz", 1965) * 1e6 / 1e12     # 4 schedulers x 1 warp-instr/cycle per SM
-        achieved = REPLAY_SWEEP_WARP_INSTR / (ms / 1e3) / 1e12
+        achieved = instr / (ms / 1e3) / 1e12
         out["roofline"] = {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "T warp-instructions/s",
-                           "frac": achieved / peak, "instructions_per_sweep": REPLAY_SWEEP_WARP_INSTR,
+                           "frac": achieved / peak, "instructions_per_sweep": instr,
+                           "instructions_per_decision": instr / max(decisions, 1),
+                           "instructions_source": "profiles/replay_sweep_launches.csv (ncu smsp__inst_executed.sum)",
                            "peak_source": "148 SMs x 4 warp schedulers x 1 instruction/cycle at sm_max_mhz"}
     if not args.no_policies:
         out["policies"] = run_policies(args, rank, world, dev)

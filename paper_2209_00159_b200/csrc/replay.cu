@@ -106,7 +106,7 @@ orloj_status replay_impl(const orloj_store *store, const orloj_latency_profile *
                     : nullptr;
     p.num_arrivals = N;
     const unsigned blocks_a = (unsigned)((p.S * G + REPLAY_WARPS - 1) / REPLAY_WARPS);
-    e = cudaMemsetAsync(ws, 0, 5 * sizeof(unsigned long long), s);  // diagnostics head (read after the call)
+    e = cudaMemsetAsync(ws, 0, 32 * sizeof(unsigned long long), s);  // diagnostics head (read after the call)
     if (e == cudaSuccess) e = launch_replay<1>(p, bpl, rate, alg1, blocks_a, smem, s);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = launch_replay<2>(p, bpl, rate, alg1, blocks, smem, s);

@@ -127,10 +127,24 @@ __host__ __device__ inline int64_t seg_log_off(int64_t arr_off_s, int64_t s, int
 }
 
 constexpr int REPLAY_WARPS = 4;
+// ORLOJ_REPLAY_STATS (diagnostic variant builds only): MODE 1 adds per-decision
+// statistics to the workspace head: [5] decisions committed by the max-plus
+// run path, [6] scanned decisions with a carried window, [7 + wc] windows of
+// wc members after the scan (wc = 0..24, 24 = 24 or more).
+#ifdef ORLOJ_REPLAY_STATS
+#define ORLOJ_STAT(i, v) do { if (MODE == 1 && lane == 0) atomicAdd(p.seg_stats + (i), (unsigned long long)(v)); } while (0)
+#else
+#define ORLOJ_STAT(i, v) do { } while (0)
+#endif
 #ifndef ORLOJ_REPLAY_KB
 #define ORLOJ_REPLAY_KB 2
 #endif
 constexpr int REPLAY_KB = ORLOJ_REPLAY_KB;  // candidate sizes per scoring block (windows are short: ~2-4)
+#ifndef ORLOJ_PAIR_MAX
+#define ORLOJ_PAIR_MAX 7
+#endif
+constexpr int PAIR_MAX = ORLOJ_PAIR_MAX;  // windows up to this size take the pair-lane path (<= 7: 28 pairs)
+static_assert(PAIR_MAX >= 1 && PAIR_MAX <= 7, "pair lanes: k (k + 1) / 2 <= 32");
 
 // Per-warp shared memory: REPLAY_KB staging rows, the window's member fields
 // and the P[k][r] matrix (row stride 36 floats: conflict-free 128-bit reads).
@@ -147,7 +161,7 @@ struct ReplayWarpSmem {
 
 // CTA shared memory: store [D][B] floats, hopeless thresholds [D] int64 (padded), warps.
 __host__ __device__ inline size_t replay_head_bytes(int D, int B) {
-  return (size_t)D * B * 4 + (size_t)((D + 1) & ~1) * 8;
+  return (((size_t)D * B * 4 + 15) & ~(size_t)15) + (size_t)((D + 1) & ~1) * 8 + 32 * 2 * 16;
 }
 
 #ifndef ORLOJ_REPLAY_MIN_BLOCKS
@@ -166,6 +180,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int D = p.D, B = p.B;
   float *s_store = s_dyn;                                                   // [D][B]
   int64_t *s_thr = reinterpret_cast<int64_t *>(s_store + (size_t)D * B);   // [D]: a_1 + w_1 m_min(d)
+  int4 *s_pair = reinterpret_cast<int4 *>(s_thr + ((D + 1) & ~1));          // [32][2] pair-lane table
   char *s_warp = reinterpret_cast<char *>(s_dyn) + replay_head_bytes(D, B);
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -184,6 +199,20 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int32_t *sm_nrec = reinterpret_cast<int32_t *>(sm_mark_base + 1);
   int32_t *sm_ext = sm_nrec + 1;
 
+  // Pair lanes for windows of 2..PAIR_MAX members (most scored windows): lane p
+  // scores candidate size pk and member pr, p = pk (pk - 1) / 2 + pr - 1, with
+  // size pk's lookup constants; as a gatherer, lane k-1 sums the pair lanes
+  // pk (pk - 1) / 2 + [0, k) of its size.  [lane][0] = {pk, pr - 1, gather base},
+  // [lane][1] = lookup constants of pk (kept in shared memory, not registers).
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    int k = 1;
+    while (k * (k + 1) / 2 <= l) ++k;  // lanes >= 28: k = 8 (idle)
+    s_pair[2 * l] = make_int4(k, l - k * (k - 1) / 2, l * (l + 1) / 2, 0);
+    s_pair[2 * l + 1] = k <= p.prof.kmax ? make_int4(p.prof.a2[k - 1], p.prof.wB2[k - 1], (int)p.prof.mag[k - 1],
+                                                     (int)p.prof.sh[k - 1])
+                                         : make_int4(0, 0, 0, 0);
+  }
   // stage the (small) store; hopeless threshold a_1 + w_1 m_min(d) per distribution
   for (int e = threadIdx.x; e < D * B; e += blockDim.x) s_store[e] = p.log2F[e];
   __syncthreads();
@@ -490,13 +519,13 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     // loop would (window of one: k* = 1, no scoring).
     if (ncarry == 0) {
       const bool va = ua != INT64_MAX;
-      const int64_t dj = a1 + w1 * ut;
       const int64_t hj = va ? ua + slo - s_thr[ud] : INT64_MIN;
       const int64_t an = __shfl_down_sync(FULL, ua, 1);
-      const int64_t t0 = __shfl_sync(FULL, ua, 0) > t ? __shfl_sync(FULL, ua, 0) : t;
-      const bool ok0 = __shfl_sync(FULL, an, 0) > t0 && t0 <= __shfl_sync(FULL, hj, 0) &&
-                       __shfl_sync(FULL, (int)va, 0);
+      // lane 0 decides for arrival `cursor` (its own registers: no broadcasts), one ballot
+      const int64_t t0 = ua > t ? ua : t;
+      const bool ok0 = __ballot_sync(FULL, lane == 0 && va && an > t0 && t0 <= hj) != 0u;
       if (ok0) {  // warp-uniform
+        const int64_t dj = a1 + w1 * ut;
         int64_t P = va ? dj : 0, Qv = va ? ua + dj : INT64_MIN;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -520,6 +549,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         c_busy += __shfl_sync(FULL, P, m - 1);
         t = __shfl_sync(FULL, Tj, m - 1);
         if (mylog && lane < m) mylog[ndec + lane] = 1;
+        ORLOJ_STAT(5, m);
         ndec += m;
         advance(m);
         continue;
@@ -529,6 +559,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     if (ncarry == 0 && next_arr > t) t = next_arr;  // idle worker: jump to the next arrival (A15)
     // ---- 1. scan -------------------------------------------------------
     int wc = 0;
+    ORLOJ_STAT(6, ncarry > 0 ? 1 : 0);
     if (ncarry > 0) {
       const bool valid = lane < ncarry;
       int64_t Dr = 0, hr = 0;
@@ -602,6 +633,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     ncarry = 0;
     carry_off = 0;
     wc = warp_uniform(wc);
+    ORLOJ_STAT(7 + (wc < 24 ? wc : 24), 1);
     __syncwarp();
     if (wc == 0) continue;
 
@@ -651,6 +683,37 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       selm = __ballot_sync(FULL, inq && rank < kstar);
     }
     if (!ALG1 && wc > 1) {   // warp-uniform
+    float E = 0.f;
+    if (!RATE && wc <= PAIR_MAX) {
+      // ---- 2'. small window: lanes over (k, r) pairs -----------------------
+      // LG_k at the pair's own lookup bin, summed over members j <= k in the
+      // block path's order (0 + x_1 + ... + x_k), then 2^LG (0 at bin 0) — the
+      // same fp32 values as the block path, and E_k from the same adder tree.
+      const int4 pq = s_pair[2 * lane], plk = s_pair[2 * lane + 1];
+      const int pk = pq.x;
+      const int sr = __shfl_sync(FULL, sig, pq.y);
+      const int bi = lookup_bin(sr, plk.x, plk.y, (uint32_t)plk.z, (uint32_t)plk.w);
+      const int bo = bi > 0 ? bi - 1 : 0;
+      float lgp = 0.f;
+#pragma unroll
+      for (int j = 0; j < PAIR_MAX; ++j) {
+        if (j >= wc) break;  // warp-uniform
+        const float x = s_store[__shfl_sync(FULL, dr, j) * B + bo];
+        if (j < pk) lgp += x;
+      }
+      const float pv = (bi > 0 && pk <= wc) ? ex2_approx(lgp) : 0.f;
+      float x[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        x[r] = 0.f;
+        if (r < PAIR_MAX && (r < 4 || wc > 4)) {  // warp-uniform
+          const float v = __shfl_sync(FULL, pv, (pq.z + r) & 31);
+          x[r] = r <= lane ? v : 0.f;
+        }
+      }
+      const float acc0 = (x[0] + x[1]) + (x[2] + x[3]);
+      E = wc <= 4 ? acc0 : acc0 + ((x[4] + x[5]) + (x[6] + x[7]));
+    } else {
     float lg[BPL];
 #pragma unroll
     for (int b = 0; b < BPL; ++b) lg[b] = 0.f;
@@ -688,20 +751,25 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
     __syncwarp();
     // E_k = sum_{r<k} P[k-1][r] in lane k-1: 128-bit row loads, adder tree
-    float E = 0.f;
     if (mem) {
       const float4 *row = reinterpret_cast<const float4 *>(Pm + lane * PST);
       const int nj = (wc + 3) >> 2;  // warp-uniform: quads holding members r < wc
       float acc[8];
+      if (nj == 1) {  // windows of <= 4 (most): the tree below reduces to its first quad, bit for bit
+        const float4 x = row[0];
+        acc[0] = (x.x + x.y) + (x.z + x.w);
+        E = acc[0];
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        acc[j] = 0.f;
-        if (j < nj && 4 * j <= lane) {
-          const float4 x = row[j];
-          acc[j] = (x.x + x.y) + (x.z + x.w);
+        for (int j = 0; j < 8; ++j) {
+          acc[j] = 0.f;
+          if (j < nj && 4 * j <= lane) {
+            const float4 x = row[j];
+            acc[j] = (x.x + x.y) + (x.z + x.w);
+          }
         }
+        E = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       }
-      E = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       if constexpr (RATE) {
         // finish rate E_k / E[L_{B_k}], E[L_{B_k}] = a_k + w_k (B - sum_{i<B} G_k(tau_i))  (Eq. 5)
         const float4 *srow = reinterpret_cast<const float4 *>(Sm + lane * PST);
@@ -715,6 +783,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         E = E / EL;
       }
     }
+    }  // block path
     // ---- 3. argmax + dispatch ----------------------------------------------
     const uint32_t mx = __reduce_max_sync(FULL, mem ? __float_as_uint(E) : 0u);
     kstar = (int)__reduce_min_sync(FULL, (mem && __float_as_uint(E) == mx) ? (uint32_t)lane : 32u) + 1;

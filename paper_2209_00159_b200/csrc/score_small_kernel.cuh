@@ -6,14 +6,17 @@
 //   LG_k[i] = LG_{k-1}[i] + log2 F_{d_k}(tau_i)   lanes over bins; rows LG_1..LG_K
 //                                                   staged in shared memory, each
 //                                                   with a -inf head for i* = 0
-//   lane k-1 then owns candidate size k: its lookup constants (a_k, w_k) sit in
-//   registers, it walks the members r = 1..k (sigma_r broadcast by shuffle) and
-//   sums  E_k = sum_{r<=k} 2^{LG_k[i*(r,k)]}  itself — no reduction tree.
+//   lane r-1 then owns member r: for k = 1..32 (unrolled, so a_k, w_k and the
+//   division magic are immediate constant-bank operands) it looks up
+//   P_r(k) = 2^{LG_k[i*(r,k)]} in row k — every lane reads the same row, so the
+//   data-dependent bins are distinct banks or broadcasts (no bank conflicts) —
+//   and pushes it into the transposing butterfly (common.cuh), which leaves
+//   E_k = sum_{r<=k} P_r(k) in lane k-1 after 31 shuffles.
 // The adds that build LG_k are the same fp32 adds in the same order as
-// score_kernel's, so LG and every P_r(k) are identical; E_k is a sequential
-// fp32 sum over r (score_kernel: a tree), within the same 1e-5 k tolerance.
-// Argmax: two REDUX (max of float bits, then min k).  Used by pick and by
-// score when neither P nor E[L_B] is requested.
+// score_kernel's, so LG and every P_r(k) are identical; E_k is the same
+// butterfly tree as score_kernel's, within the 1e-5 k tolerance.  Argmax: two
+// REDUX (max of float bits, then min k).  Used by pick and by score when
+// neither P nor E[L_B] is requested.
 #pragma once
 #include "common.cuh"
 #include "score_kernel.cuh"
@@ -22,10 +25,10 @@ namespace orloj {
 
 constexpr int SMALL_WARPS = 8;
 
-// shared memory: store [D][B] | profile int4 [32] | per warp LG rows [32][32 BPL + 1]
+// shared memory: store [D][B] | lookup constants int4 [32] | per warp LG rows [32][32 BPL + 1]
 template <int BPL>
 struct SmallShape {
-  static constexpr int ROW = 32 * BPL + 1;  // odd row stride: rows start on different banks
+  static constexpr int ROW = 32 * BPL + 1;  // row k-1: [0] = -inf (i* = 0), [i] = LG_k(tau_i)
   __host__ __device__ static size_t bytes(int D, int B) {
     return (((size_t)D * B * 4 + 15) & ~(size_t)15) + 32 * 16 + (size_t)SMALL_WARPS * 32 * ROW * 4;
   }
@@ -40,13 +43,15 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   const int D = p.D, B = p.B, kmax = p.kmax;
   float *s_store = s_dyn;
   int4 *s_prof = reinterpret_cast<int4 *>(s_dyn + (((size_t)D * B + 3) & ~(size_t)3));
-  float *lgs = reinterpret_cast<float *>(s_prof + 32) + wid * 32 * ROW;  // row k-1 = LG_k; [0] = -inf
+  float *lgs = reinterpret_cast<float *>(s_prof + 32) + wid * 32 * ROW;  // row k-1 = LG_k
 
   for (int e = threadIdx.x * 4; e < D * B; e += blockDim.x * 4)
     *reinterpret_cast<float4 *>(s_store + e) = __ldg(reinterpret_cast<const float4 *>(p.log2F + e));
-  if (threadIdx.x < kmax)
-    s_prof[threadIdx.x] = make_int4(p.prof.a2[threadIdx.x], p.prof.wB2[threadIdx.x], (int)p.prof.mag[threadIdx.x],
-                                    (int)p.prof.sh[threadIdx.x]);
+  if (threadIdx.x < 32) {  // sizes beyond kmax: constants that look up bin 0 (never counted)
+    const int k = threadIdx.x;
+    s_prof[k] = k < kmax ? make_int4(p.prof.a2[k], p.prof.wB2[k], (int)p.prof.mag[k], (int)p.prof.sh[k])
+                         : make_int4(0, 0, 0, 0);
+  }
   lgs[lane * ROW] = -INFINITY;
   __syncthreads();
 
@@ -58,7 +63,6 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   const int64_t now = p.now[q];
   const int32_t sig = lane < K ? sigma2(p.deadline[off + lane] - now) : 0;
   const int idB = lane < K ? p.dist[off + lane] * B : 0;  // row offset of member lane's distribution
-  const int4 pk = s_prof[lane < kmax ? lane : 0];
 
   // a2: LG_k for k = 1..K, lanes over bins (bin lane + 32 e + 1)
   float acc[BPL];
@@ -82,21 +86,19 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   }
   __syncwarp();
 
-  // a3-a5: lane k-1 sums P_r(k) over its members r = 1..k
-  const float *row = lgs + lane * ROW;
+  // a3-a5: lane r-1 looks up its member in every row k (constants of size k:
+  // one broadcast 128-bit load); the butterfly sums over r.  Rows k > K were
+  // not built: their lookups are computed but masked (lane < k <= K).
+  const uint32_t row0 = smem_addr(lgs);
+  float pend[5];
   float E = 0.f;
-  int r = 0;
-  for (; r + 4 <= K; r += 4) {
-    float v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      v[j] = ex2_approx(row[lookup_bin(__shfl_sync(FULL, sig, r + j), pk.x, pk.y, (uint32_t)pk.z, (uint32_t)pk.w)]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) E += r + j <= lane ? v[j] : 0.f;
-  }
-  for (; r < K; ++r) {
-    const float v = ex2_approx(row[lookup_bin(__shfl_sync(FULL, sig, r), pk.x, pk.y, (uint32_t)pk.z, (uint32_t)pk.w)]);
-    E += r <= lane ? v : 0.f;
+  for (int k = 1; k <= 32; ++k) {
+    const int4 c = s_prof[k - 1];
+    const int bi = lookup_bin(sig, c.x, c.y, (uint32_t)c.z, (uint32_t)c.w);
+    const float x = ex2_approx(lds_f32(row0 + 4u * (uint32_t)((k - 1) * ROW + bi)));
+    const float v = (lane < k && k <= K) ? x : 0.f;  // members r <= k (lanes >= K hold no member)
+    E = bfly_push(pend, v, k - 1, lane);
   }
 
   // a6: argmax, ties -> smallest k (E >= 0: float bits order like values)

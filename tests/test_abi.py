@@ -21,7 +21,7 @@ def lib():
 def _declared():
     src = open(_abi.HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(orloj_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(orloj_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_symbols_exported(lib):
