@@ -148,6 +148,82 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
+// ---- 32-bit shared-space arrays -------------------------------------------
+// A generic pointer into dynamic shared memory makes the compiler rebuild the
+// CTA's shared window base (S2UR CgaCtaId, ULEA, ...) at every access of a hot
+// loop rather than spend a register on it; a 32-bit shared-space address kept
+// in one register and explicit ld/st.shared avoid that.  smem_base() returns
+// the address through an opaque move so it is computed once.
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  asm volatile("mov.u32 %0, %1;" : "=r"(x) : "r"(x));
+  return x;
+}
+__device__ __forceinline__ uint32_t smem_base(const void *p) { return opaque_u32(smem_addr(p)); }
+
+template <class T> struct SArr;
+template <> struct SArr<int64_t> {
+  uint32_t a;
+  __device__ __forceinline__ int64_t ld(int i) const {
+    int64_t v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a + 8u * (uint32_t)i) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ void st(int i, int64_t v) const {
+    asm volatile("st.shared.s64 [%0], %1;" ::"r"(a + 8u * (uint32_t)i), "l"(v) : "memory");
+  }
+};
+template <> struct SArr<int32_t> {
+  uint32_t a;
+  __device__ __forceinline__ int32_t ld(int i) const {
+    int32_t v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a + 4u * (uint32_t)i) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ void st(int i, int32_t v) const {
+    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a + 4u * (uint32_t)i), "r"(v) : "memory");
+  }
+};
+template <> struct SArr<float> {
+  uint32_t a;
+  __device__ __forceinline__ float ld(int i) const {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a + 4u * (uint32_t)i) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ void st(int i, float v) const {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a + 4u * (uint32_t)i), "f"(v) : "memory");
+  }
+  // V consecutive floats starting at element i (4V-byte aligned)
+  template <int V>
+  __device__ __forceinline__ void ldv(int i, float (&x)[V]) const {
+    const uint32_t ad = a + 4u * (uint32_t)i;
+    if constexpr (V == 4)
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]) : "r"(ad)
+                   : "memory");
+    else if constexpr (V == 2)
+      asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(x[0]), "=f"(x[1]) : "r"(ad) : "memory");
+    else
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(ad) : "memory");
+  }
+  template <int V>
+  __device__ __forceinline__ void stv(int i, const float *x) const {
+    const uint32_t ad = a + 4u * (uint32_t)i;
+    if constexpr (V == 4)
+      asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(ad), "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3])
+                   : "memory");
+    else if constexpr (V == 2)
+      asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(ad), "f"(x[0]), "f"(x[1]) : "memory");
+    else
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(ad), "f"(x[0]) : "memory");
+  }
+};
+__device__ __forceinline__ int4 lds_v4s32(uint32_t a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }

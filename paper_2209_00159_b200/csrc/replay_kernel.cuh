@@ -185,19 +185,28 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   char *my = s_warp + wid * ReplayWarpSmem<BPL, RATE>::bytes();
-  float *stg = reinterpret_cast<float *>(my) + 4;                            // REPLAY_KB rows, stride STG
-  int64_t *w_dl = reinterpret_cast<int64_t *>(my + REPLAY_KB * STG * 4);    // window deadlines
-  int64_t *w_h = w_dl + 32;                                                 // window hopeless times
-  int32_t *w_d = reinterpret_cast<int32_t *>(w_h + 32);                     // window distributions
-  int32_t *w_tb = w_d + 32;                                                 // window true bins
-  int32_t *w_ix = w_tb + 32;  // window arrival indices (MODE 0 with per-arrival outcomes only)
-  float *Pm = reinterpret_cast<float *>(w_ix + 32);                         // P[k-1][r], stride PST
-  float *Sm = Pm + 32 * PST;  // RATE only: per-lane partial sum_{i<B} G_k(tau_i), [k-1][lane]
+  float *stg_p = reinterpret_cast<float *>(my) + 4;                          // REPLAY_KB rows, stride STG
+  // the loop addresses shared memory through 32-bit shared-space arrays (common.cuh SArr)
+  const uint32_t sb = smem_base(s_dyn);
+  const uint32_t mb0 =
+      opaque_u32(sb + (uint32_t)replay_head_bytes(D, B) + (uint32_t)wid * (uint32_t)ReplayWarpSmem<BPL, RATE>::bytes());
+  const SArr<float> sto{sb};                                                 // store [D][B]
+  const SArr<int64_t> thr{opaque_u32(sb + (uint32_t)D * B * 4)};             // [D]: a_1 + w_1 m_min(d)
+  const uint32_t a_pair = opaque_u32(thr.a + (uint32_t)((D + 1) & ~1) * 8);  // [32][2] int4
+  const SArr<float> stg{mb0 + 16};                                            // REPLAY_KB rows, stride STG
+  const uint32_t a_win = mb0 + REPLAY_KB * STG * 4;
+  const SArr<int64_t> w_dl{a_win};               // window deadlines
+  const SArr<int64_t> w_h{a_win + 256};          // window hopeless times
+  const SArr<int32_t> w_d{a_win + 512};          // window distributions
+  const SArr<int32_t> w_tb{a_win + 640};         // window true bins
+  const SArr<int32_t> w_ix{a_win + 768};         // window arrival indices (MODE 0 with per-arrival outcomes)
+  const SArr<float> Pm{a_win + 896};             // P[k-1][r], stride PST
+  const SArr<float> Sm{a_win + 896 + 32 * PST * 4};  // RATE only: per-lane partial sum_{i<B} G_k(tau_i), [k-1][lane]
   // MODE 1 (cold, warp-uniform; kept out of registers): base arrival of the
   // current record list, records in it, extension flag
-  int64_t *sm_mark_base = reinterpret_cast<int64_t *>(Sm + (RATE ? 32 * PST : 0));
-  int32_t *sm_nrec = reinterpret_cast<int32_t *>(sm_mark_base + 1);
-  int32_t *sm_ext = sm_nrec + 1;
+  const SArr<int64_t> sm_mark_base{a_win + 896 + (RATE ? 2 : 1) * 32 * PST * 4};
+  const SArr<int32_t> sm_nrec{a_win + 896 + (RATE ? 2 : 1) * 32 * PST * 4 + 8};
+  const SArr<int32_t> sm_ext{a_win + 896 + (RATE ? 2 : 1) * 32 * PST * 4 + 12};
 
   // Pair lanes for windows of 2..PAIR_MAX members (most scored windows): lane p
   // scores candidate size pk and member pr, p = pk (pk - 1) / 2 + pr - 1, with
@@ -223,7 +232,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     s_thr[d] = ALG1 ? p.size_thr[0]  // Alg. 1 l.10-13: infeasible for every bs iff infeasible for bs = 1
                     : p.drop_thr ? p.drop_thr[d] : (int64_t)p.prof.a[0] + (int64_t)p.prof.w[0] * m;
   }
-  if (lane < REPLAY_KB) stg[lane * STG - 1] = -INFINITY;
+  if (lane < REPLAY_KB) stg_p[lane * STG - 1] = -INFINITY;
   __syncthreads();
 
   if constexpr (MODE != 0) {
@@ -284,9 +293,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     cursor = seg_begin(n, g, p.G);
     if (g > 0) rec_at = cursor;  // segment 0's records are never matched
     if (lane == 0) {
-      *sm_mark_base = cursor;
-      *sm_nrec = 0;
-      *sm_ext = 0;
+      sm_mark_base.st(0, cursor);
+      sm_nrec.st(0, 0);
+      sm_ext.st(0, 0);
     }
     __syncwarp();
     if (g + 1 < p.G) seg_end = seg_begin(n, g + 1, p.G);
@@ -316,10 +325,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   // MODE 1: end state of the segment run
   auto save_end = [&]() {
     if (lane < ncarry) {
-      sg->carry_D[lane] = w_dl[carry_off + lane];
-      sg->carry_h[lane] = w_h[carry_off + lane];
-      sg->carry_d[lane] = w_d[carry_off + lane];
-      sg->carry_tb[lane] = w_tb[carry_off + lane];
+      sg->carry_D[lane] = w_dl.ld(carry_off + lane);
+      sg->carry_h[lane] = w_h.ld(carry_off + lane);
+      sg->carry_d[lane] = w_d.ld(carry_off + lane);
+      sg->carry_tb[lane] = w_tb.ld(carry_off + lane);
     }
     if (lane == 0) {
       sg->t = t;
@@ -360,10 +369,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     carry_off = 0;
     __syncwarp();
     if (lane < ncarry) {
-      w_dl[lane] = e->carry_D[lane];
-      w_h[lane] = e->carry_h[lane];
-      w_d[lane] = e->carry_d[lane];
-      w_tb[lane] = e->carry_tb[lane];
+      w_dl.st(lane, e->carry_D[lane]);
+      w_h.st(lane, e->carry_h[lane]);
+      w_d.st(lane, e->carry_d[lane]);
+      w_tb.st(lane, e->carry_tb[lane]);
     }
     __syncwarp();
     reload();
@@ -442,15 +451,15 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   while (cursor < n || ncarry > 0) {
     if constexpr (MODE == 1) {
       if (cursor >= seg_end) {  // first loop top past the segment: its end state, then the extension
-        if (*sm_ext) break;
-        nrec = *sm_nrec;
+        if (sm_ext.ld(0)) break;
+        nrec = sm_nrec.ld(0);
         save_end();
         rec_at = seg_end;
         __syncwarp();
         if (lane == 0) {
-          *sm_ext = 1;
-          *sm_mark_base = seg_end;
-          *sm_nrec = 0;
+          sm_ext.st(0, 1);
+          sm_mark_base.st(0, seg_end);
+          sm_nrec.st(0, 0);
         }
         __syncwarp();
         seg_end = seg_begin(n, g + 2, p.G);
@@ -461,9 +470,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       if (cursor >= rec_at && ncarry == 0) {
         const int64_t a0 = __shfl_sync(FULL, ua, 0);
         if (a0 != INT64_MAX && t <= a0) {  // regeneration point at arrival `cursor`: record it
-          const int nr = *sm_nrec;
-          const bool ext = *sm_ext;
-          const int64_t mb = *sm_mark_base;
+          const int nr = sm_nrec.ld(0);
+          const bool ext = sm_ext.ld(0);
+          const int64_t mb = sm_mark_base.ld(0);
           const long long v = lane == 0 ? cursor : lane == 1 ? ndec : lane == 2 ? c_fin : lane == 3 ? c_drop
                               : lane == 4 ? c_late : lane == 5 ? c_bat : c_busy;
           if (lane < 7) reinterpret_cast<long long *>(ext ? &sg->ext[nr] : &sg->rec[nr])[lane] = v;
@@ -471,7 +480,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
           while (m <= cursor - mb) m = seg_next_mark(m);
           rec_at = nr + 1 < SEG_REC ? mb + m : INT64_MAX;
           __syncwarp();
-          if (lane == 0) *sm_nrec = nr + 1;
+          if (lane == 0) sm_nrec.st(0, nr + 1);
           __syncwarp();
           if (ext && nr + 1 > SEG_EXT_AFTER) break;
         }
@@ -519,7 +528,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     // loop would (window of one: k* = 1, no scoring).
     if (ncarry == 0) {
       const bool va = ua != INT64_MAX;
-      const int64_t hj = va ? ua + slo - s_thr[ud] : INT64_MIN;
+      const int64_t hj = va ? ua + slo - thr.ld(ud) : INT64_MIN;
       const int64_t an = __shfl_down_sync(FULL, ua, 1);
       // lane 0 decides for arrival `cursor` (its own registers: no broadcasts), one ballot
       const int64_t t0 = ua > t ? ua : t;
@@ -565,11 +574,11 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       int64_t Dr = 0, hr = 0;
       int dr = 0, tr = 0, ir = 0;
       if (valid) {
-        Dr = w_dl[carry_off + lane];
-        hr = w_h[carry_off + lane];
-        dr = w_d[carry_off + lane];
-        tr = w_tb[carry_off + lane];
-        if (oc) ir = w_ix[carry_off + lane];
+        Dr = w_dl.ld(carry_off + lane);
+        hr = w_h.ld(carry_off + lane);
+        dr = w_d.ld(carry_off + lane);
+        tr = w_tb.ld(carry_off + lane);
+        if (oc) ir = w_ix.ld(carry_off + lane);
       }
       const bool keep = valid && t <= hr;
       const unsigned vm = __ballot_sync(FULL, valid);
@@ -579,11 +588,11 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       __syncwarp();
       if (keep) {
         const int slot = __popc(km & ((1u << lane) - 1u));
-        w_dl[slot] = Dr;
-        w_h[slot] = hr;
-        w_d[slot] = dr;
-        w_tb[slot] = tr;
-        if (oc) w_ix[slot] = ir;
+        w_dl.st(slot, Dr);
+        w_h.st(slot, hr);
+        w_d.st(slot, dr);
+        w_tb.st(slot, tr);
+        if (oc) w_ix.st(slot, ir);
       }
       wc = __popc(km);
     }
@@ -591,7 +600,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const bool valid = ua <= t;  // arrivals are sorted: valid lanes form a prefix
       const unsigned vm = __ballot_sync(FULL, valid);
       if (vm == 0) break;
-      const int64_t uh = ua + slo - s_thr[ud];  // hopeless time (computed here: refilled lanes' loads
+      const int64_t uh = ua + slo - thr.ld(ud);  // hopeless time (computed here: refilled lanes' loads
       const bool keep = valid && t <= uh;        // are never consumed in the decision that issued them)
       const unsigned km = __ballot_sync(FULL, keep);
       const int need = kmax - wc;
@@ -608,11 +617,11 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       if (oc && ((vm & consumed & ~km) >> lane) & 1u) oc[cursor + lane] = 3;
       if ((kc >> lane) & 1u) {
         const int slot = wc + __popc(kc & ((1u << lane) - 1u));
-        w_dl[slot] = ua + slo;
-        w_h[slot] = uh;
-        w_d[slot] = ud;
-        w_tb[slot] = ut;
-        if (oc) w_ix[slot] = (int32_t)(cursor + lane);
+        w_dl.st(slot, ua + slo);
+        w_h.st(slot, uh);
+        w_d.st(slot, ud);
+        w_tb.st(slot, ut);
+        if (oc) w_ix.st(slot, (int32_t)(cursor + lane));
       }
       wc += __popc(kc);
       const int nc = __popc(consumed);
@@ -639,10 +648,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
 
     // ---- 2. score the window ---------------------------------------------
     const bool mem = lane < wc;
-    const int64_t Dr = mem ? w_dl[lane] : 0;
+    const int64_t Dr = mem ? w_dl.ld(lane) : 0;
     const int32_t sig = mem ? sigma2(Dr - t) : 0;
-    const int dr = mem ? w_d[lane] : 0;
-    const int tb = mem ? w_tb[lane] : 0;
+    const int dr = mem ? w_d.ld(lane) : 0;
+    const int tb = mem ? w_tb.ld(lane) : 0;
 
     int kstar = 1;  // a window of one has a single candidate: no scoring needed
     uint32_t selm = 1u;  // ALG1: the popped members (window positions)
@@ -653,12 +662,12 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const int64_t need = my_thr == INT64_MAX ? INT64_MAX : t + my_thr;  // beyond kmax: never feasible
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (w_dl[mid] < need || my_thr == INT64_MAX) lo = mid + 1;
+        if (w_dl.ld(mid) < need || my_thr == INT64_MAX) lo = mid + 1;
         else hi = mid;
       }
       const bool feas = lane < kmax && wc - lo >= lane + 1;  // |Q_bs| >= bs
       // candidate: earliest D_{Q_bs}, ties -> larger bs (SURVEY A/Design reading of P:296-297)
-      const uint64_t dq = feas ? (uint64_t)(w_dl[lo] - t) : ~0ull;  // >= 0 when feasible
+      const uint64_t dq = feas ? (uint64_t)(w_dl.ld(lo) - t) : ~0ull;  // >= 0 when feasible
       const uint32_t mh = __reduce_min_sync(FULL, (uint32_t)(dq >> 32));
       const uint32_t ml = __reduce_min_sync(FULL, (uint32_t)(dq >> 32) == mh ? (uint32_t)dq : 0xffffffffu);
       kstar = (int)__reduce_max_sync(FULL, (feas && dq == (((uint64_t)mh << 32) | ml)) ? (uint32_t)(lane + 1) : 0u);
@@ -689,7 +698,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       // LG_k at the pair's own lookup bin, summed over members j <= k in the
       // block path's order (0 + x_1 + ... + x_k), then 2^LG (0 at bin 0) — the
       // same fp32 values as the block path, and E_k from the same adder tree.
-      const int4 pq = s_pair[2 * lane], plk = s_pair[2 * lane + 1];
+      const int4 pq = lds_v4s32(a_pair + 32u * lane), plk = lds_v4s32(a_pair + 32u * lane + 16u);
       const int pk = pq.x;
       const int sr = __shfl_sync(FULL, sig, pq.y);
       const int bi = lookup_bin(sr, plk.x, plk.y, (uint32_t)plk.z, (uint32_t)plk.w);
@@ -698,7 +707,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
 #pragma unroll
       for (int j = 0; j < PAIR_MAX; ++j) {
         if (j >= wc) break;  // warp-uniform
-        const float x = s_store[__shfl_sync(FULL, dr, j) * B + bo];
+        const float x = sto.ld(__shfl_sync(FULL, dr, j) * B + bo);
         if (j < pk) lgp += x;
       }
       const float pv = (bi > 0 && pk <= wc) ? ex2_approx(lgp) : 0.f;
@@ -726,18 +735,19 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       for (int i = 0; i < REPLAY_KB; ++i) {
         const int d = __shfl_sync(FULL, dr, (k0 + i) & 31);  // beyond wc: harmless id 0
         if (vok) {
-          const Vec<BPL> x = *reinterpret_cast<const Vec<BPL> *>(s_store + d * B + lane * BPL);
+          float x[BPL];
+          sto.ldv<BPL>(d * B + lane * BPL, x);
 #pragma unroll
-          for (int e = 0; e < BPL; ++e) lg[e] += x.x[e];
+          for (int e = 0; e < BPL; ++e) lg[e] += x[e];
         }
-        st_vec<BPL>(stg + i * STG + lane * BPL, lg);
+        stg.stv<BPL>(i * STG + lane * BPL, lg);
         if constexpr (RATE) {
           // this lane's share of sum_{i<B} G_k(tau_i) (bins tau_1 .. tau_{B-1})
           float part = 0.f;
 #pragma unroll
           for (int e = 0; e < BPL; ++e)
             if (lane * BPL + e < B - 1) part += ex2_approx(lg[e]);
-          Sm[((k0 + i) & 31) * PST + lane] = part;
+          Sm.st(((k0 + i) & 31) * PST + lane, part);
         }
       }
       __syncwarp();
@@ -745,38 +755,39 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       for (int i = 0; i < REPLAY_KB; ++i) {
         const int kk = k0 + i;  // k - 1 (rows at or beyond wc are computed but never read)
         const int bi = lookup_bin(sig, p.prof.a2[kk], p.prof.wB2[kk], p.prof.mag[kk], p.prof.sh[kk]);
-        const float pr = ex2_approx(stg[i * STG + bi - 1]);
-        Pm[(kk & 31) * PST + lane] = lane <= kk ? pr : 0.f;
+        const float pr = ex2_approx(stg.ld(i * STG + bi - 1));
+        Pm.st((kk & 31) * PST + lane, lane <= kk ? pr : 0.f);
       }
     }
     __syncwarp();
     // E_k = sum_{r<k} P[k-1][r] in lane k-1: 128-bit row loads, adder tree
     if (mem) {
-      const float4 *row = reinterpret_cast<const float4 *>(Pm + lane * PST);
       const int nj = (wc + 3) >> 2;  // warp-uniform: quads holding members r < wc
       float acc[8];
-      if (nj == 1) {  // windows of <= 4 (most): the tree below reduces to its first quad, bit for bit
-        const float4 x = row[0];
-        acc[0] = (x.x + x.y) + (x.z + x.w);
+      if (nj == 1) {  // windows of <= 4: the tree below reduces to its first quad, bit for bit
+        float x[4];
+        Pm.ldv<4>(lane * PST, x);
+        acc[0] = (x[0] + x[1]) + (x[2] + x[3]);
         E = acc[0];
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           acc[j] = 0.f;
           if (j < nj && 4 * j <= lane) {
-            const float4 x = row[j];
-            acc[j] = (x.x + x.y) + (x.z + x.w);
+            float x[4];
+            Pm.ldv<4>(lane * PST + 4 * j, x);
+            acc[j] = (x[0] + x[1]) + (x[2] + x[3]);
           }
         }
         E = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
       }
       if constexpr (RATE) {
         // finish rate E_k / E[L_{B_k}], E[L_{B_k}] = a_k + w_k (B - sum_{i<B} G_k(tau_i))  (Eq. 5)
-        const float4 *srow = reinterpret_cast<const float4 *>(Sm + lane * PST);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float4 x = srow[j];
-          acc[j] = (x.x + x.y) + (x.z + x.w);
+          float x[4];
+          Sm.ldv<4>(lane * PST + 4 * j, x);
+          acc[j] = (x[0] + x[1]) + (x[2] + x[3]);
         }
         const float S = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         const float EL = my_a + my_w * ((float)B - S);
@@ -795,7 +806,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
                                    (int64_t)__shfl_sync(FULL, my_wk, kstar - 1) * mbin
                              : (int64_t)p.prof.a[kstar - 1] + (int64_t)p.prof.w[kstar - 1] * mbin;
     const unsigned fm = __ballot_sync(FULL, sel && t + dur <= Dr);
-    const int ix = (oc && mem) ? w_ix[lane] : 0;
+    const int ix = (oc && mem) ? w_ix.ld(lane) : 0;
     if (oc && sel) oc[ix] = ((fm >> lane) & 1u) ? 1 : 2;
     c_fin += __popc(fm);
     c_late += kstar - __popc(fm);
@@ -808,24 +819,24 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     carry_off = kstar;
     if (ALG1 && ncarry > 0) {
       // the unpopped members stay pending in deadline order: compact in place
-      const int64_t hr = mem ? w_h[lane] : 0;
+      const int64_t hr = mem ? w_h.ld(lane) : 0;
       const unsigned km = __ballot_sync(FULL, mem && !sel);
       __syncwarp();
       if (mem && !sel) {
         const int slot = __popc(km & ((1u << lane) - 1u));
-        w_dl[slot] = Dr;
-        w_h[slot] = hr;
-        w_d[slot] = dr;
-        w_tb[slot] = tb;
-        if (oc) w_ix[slot] = ix;
+        w_dl.st(slot, Dr);
+        w_h.st(slot, hr);
+        w_d.st(slot, dr);
+        w_tb.st(slot, tb);
+        if (oc) w_ix.st(slot, ix);
       }
       carry_off = 0;
     }
     __syncwarp();
   }
   if constexpr (MODE == 1) {
-    const bool ext = *sm_ext;
-    nrec = *sm_nrec;
+    const bool ext = sm_ext.ld(0);
+    nrec = sm_nrec.ld(0);
     if (!ext) save_end();  // ended before s_{g+1} (last segment, or the trace ran out)
     if (lane == 0) {
       sg->next = ext ? nrec : 0;

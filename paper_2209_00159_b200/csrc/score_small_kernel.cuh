@@ -87,8 +87,9 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   __syncwarp();
 
   // a3-a5: lane r-1 looks up its member in every row k (constants of size k:
-  // one broadcast 128-bit load); the butterfly sums over r.  Rows k > K were
-  // not built: their lookups are computed but masked (lane < k <= K).
+  // one broadcast 128-bit load); the butterfly sums over r.  Lanes >= K hold
+  // sigma = 0, i.e. bin 0 and P = 0; rows k > K were not built, but they only
+  // reach E_k for k > K, which is never used.
   const uint32_t row0 = smem_addr(lgs);
   float pend[5];
   float E = 0.f;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
     const int4 c = s_prof[k - 1];
     const int bi = lookup_bin(sig, c.x, c.y, (uint32_t)c.z, (uint32_t)c.w);
     const float x = ex2_approx(lds_f32(row0 + 4u * (uint32_t)((k - 1) * ROW + bi)));
-    const float v = (lane < k && k <= K) ? x : 0.f;  // members r <= k (lanes >= K hold no member)
+    const float v = lane < k ? x : 0.f;  // members r <= k
     E = bfly_push(pend, v, k - 1, lane);
   }
 
