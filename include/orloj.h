@@ -215,7 +215,10 @@ typedef struct {
  * per_bucket: device [num_buckets]; counters are ADDED (atomics), so zero them
  * first.  decision_log: device int32 [N + S] or NULL; decision d of scenario s
  * is written at [arrival_offsets[s] + s + d], followed by a 0.
- * Limits: kmax <= 32, B <= 128, D*B*4 <= 64 KiB (CAPACITY otherwise). */
+ * Limits: kmax <= 32, B <= 128, D*B*4 <= 64 KiB (CAPACITY otherwise); every
+ * scenario holds fewer than 2^31 - 64 arrivals (per-scenario indices and counts
+ * are 32-bit in the kernel; orloj_validate_trace checks it, and a replay that
+ * meets a longer scenario faults: ORLOJ_ERR_CUDA at the next synchronisation). */
 orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
                                 const orloj_trace *trace, orloj_counters *per_bucket,
                                 int32_t *decision_log, void *stream);
@@ -491,8 +494,9 @@ orloj_status orloj_validate_store(const orloj_store *store, void *stream);
 /* offsets monotone from 0; dist ids in range (INVALID_ARGUMENT); per-queue
  * (deadline, arrival, index) order (UNSORTED; arrival used when non-NULL). */
 orloj_status orloj_validate_queues(const orloj_store *store, const orloj_queues *queues, void *stream);
-/* offsets monotone from 0, ids / bins / buckets in range, slo >= 0 (INVALID_ARGUMENT);
- * arrivals non-decreasing per scenario (UNSORTED). */
+/* offsets monotone from 0, ids / bins / buckets in range, slo >= 0, fewer than
+ * 2^31 - 64 arrivals per scenario (INVALID_ARGUMENT); arrivals non-decreasing
+ * per scenario (UNSORTED). */
 orloj_status orloj_validate_trace(const orloj_store *store, const orloj_trace *trace, void *stream);
 
 #ifdef __cplusplus

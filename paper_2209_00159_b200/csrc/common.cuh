@@ -30,9 +30,11 @@ struct ProfileDev {
 // <= 0 there); above, the horizon a_kmax + w_kmax B <= 2^30 - 1 (checked on the
 // host) makes every lookup saturate at B already.
 __device__ __forceinline__ int32_t sigma2(int64_t sigma) {
-  sigma = sigma < 0 ? 0 : sigma;
-  sigma = sigma > 0x3fffffffLL ? 0x3fffffffLL : sigma;
-  return (int32_t)(2 * sigma);
+  // on the two 32-bit halves: negative -> 0, >= 2^32 -> the cap, else min(lo, cap)
+  const int32_t hi = (int32_t)(sigma >> 32);
+  const uint32_t lo = (uint32_t)sigma;
+  const uint32_t c = hi < 0 ? 0u : hi > 0 ? 0x3fffffffu : min(lo, 0x3fffffffu);
+  return (int32_t)(2u * c);
 }
 
 // Eq. 3-4 + Eq. 9 (CDF form): i*(r,k) = clamp(floor((sigma - a_k) / w_k), 0, B)

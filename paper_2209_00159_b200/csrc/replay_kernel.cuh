@@ -182,7 +182,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int64_t *s_thr = reinterpret_cast<int64_t *>(s_store + (size_t)D * B);   // [D]: a_1 + w_1 m_min(d)
   int4 *s_pair = reinterpret_cast<int4 *>(s_thr + ((D + 1) & ~1));          // [32][2] pair-lane table
   char *s_warp = reinterpret_cast<char *>(s_dyn) + replay_head_bytes(D, B);
-  const int lane = threadIdx.x & 31;
+  const int lane = (int)opaque_u32(threadIdx.x & 31);  // pinned: not re-read from SR_TID in the loop
   const int wid = threadIdx.x >> 5;
   char *my = s_warp + wid * ReplayWarpSmem<BPL, RATE>::bytes();
   float *stg_p = reinterpret_cast<float *>(my) + 4;                          // REPLAY_KB rows, stride STG
@@ -266,6 +266,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
     if (p.outcome) oc = p.outcome + base;
   }
+  // per-scenario indices and counts are 32-bit (include/orloj.h: a scenario
+  // holds fewer than 2^31 - 64 arrivals; a violated precondition is a fault)
+  if (n > 0x7fffffbfll) __trap();
+  const int32_t ni = (int32_t)n;
   const int64_t slo = p.slo[s];
   const int64_t *arr = p.arrival + base;
   const int32_t *dis = p.dist + base;
@@ -284,13 +288,13 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int64_t t = INT64_MIN;
   if constexpr (MODE == 0)
     if (p.t_carry) t = p.t_carry[s];  // the worker is busy until then (INT64_MIN: free)
-  int64_t cursor = 0;
-  int64_t seg_end = INT64_MAX;  // MODE 1: stop (s_{g+1}, then the extension cap); MODE 2: s_{g+1} of the stitched g
-  int64_t rec_at = INT64_MAX;  // MODE 1: record the first regeneration point at or past this arrival
+  int32_t cursor = 0;
+  int32_t seg_end = INT32_MAX;  // MODE 1: stop (s_{g+1}, then the extension cap); MODE 2: s_{g+1} of the stitched g
+  int32_t rec_at = INT32_MAX;  // MODE 1: record the first regeneration point at or past this arrival
   ReplaySeg *sg = nullptr;               // MODE 1: this segment; MODE 2: the scenario's segments
   int32_t *mylog = p.log ? p.log + base + s : nullptr;
   if constexpr (MODE == 1) {
-    cursor = seg_begin(n, g, p.G);
+    cursor = (int32_t)seg_begin(n, g, p.G);
     if (g > 0) rec_at = cursor;  // segment 0's records are never matched
     if (lane == 0) {
       sm_mark_base.st(0, cursor);
@@ -298,7 +302,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       sm_ext.st(0, 0);
     }
     __syncwarp();
-    if (g + 1 < p.G) seg_end = seg_begin(n, g + 1, p.G);
+    if (g + 1 < p.G) seg_end = (int32_t)seg_begin(n, g + 1, p.G);
     sg = p.seg + u;
     if (g > 0) mylog = p.seg_log ? p.seg_log + seg_log_off(base, s, n, g, p.G) : nullptr;
   }
@@ -306,9 +310,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int64_t ua = INT64_MAX;
   int ud = 0, ut = 0;
   auto reload = [&]() {
-    const int64_t idx = cursor + lane;
+    const int32_t idx = cursor + lane;
     ua = INT64_MAX;
-    if (idx < n) {
+    if (idx < ni) {
       ua = arr[idx];
       ud = dis[idx];
       ut = tbs[idx];
@@ -316,8 +320,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   };
   reload();
   int ncarry = 0, carry_off = 0;
-  long long c_fin = 0, c_drop = 0, c_late = 0, c_bat = 0, c_busy = 0;
-  int64_t ndec = 0;
+  uint32_t c_fin = 0, c_drop = 0, c_late = 0, c_bat = 0;  // < 2^32: counts within one scenario
+  long long c_busy = 0;
+  int32_t ndec = 0;
   int nrec = 0;  // MODE 1: records in the current list; MODE 2: match pointer into segment g's records
   int64_t taken = 0;  // MODE 2: decisions taken over from segment runs (the rest were re-run here)
   int joined = 0, crossed = 0;
@@ -353,18 +358,18 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const int32_t *src = seg_src_log(gg);
       for (long long i = from + lane; i < to; i += 32) mylog[ndec + i - from] = src[i];
     }
-    c_fin += c1[0] - c0[0];
-    c_drop += c1[1] - c0[1];
-    c_late += c1[2] - c0[2];
-    c_bat += c1[3] - c0[3];
+    c_fin += (uint32_t)(c1[0] - c0[0]);
+    c_drop += (uint32_t)(c1[1] - c0[1]);
+    c_late += (uint32_t)(c1[2] - c0[2]);
+    c_bat += (uint32_t)(c1[3] - c0[3]);
     c_busy += c1[4] - c0[4];
-    ndec += to - from;
+    ndec += (int32_t)(to - from);
     taken += to - from;
   };
   // MODE 2: load segment gg's end state into the registers / window (the true state)
   auto materialize = [&](const ReplaySeg *e) {
     t = e->t;
-    cursor = e->cursor;
+    cursor = (int32_t)e->cursor;
     ncarry = e->ncarry;
     carry_off = 0;
     __syncwarp();
@@ -407,20 +412,20 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   if constexpr (MODE == 2) {
     // segment 0 ran from the true start: the true run is at its end state
     sg = p.seg + s * p.G;
-    ndec = sg[0].ndec;  // segment 0 wrote its decisions into the true log
+    ndec = (int32_t)sg[0].ndec;  // segment 0 wrote its decisions into the true log
     taken = ndec;
-    c_fin = sg[0].ctr[0];
-    c_drop = sg[0].ctr[1];
-    c_late = sg[0].ctr[2];
-    c_bat = sg[0].ctr[3];
+    c_fin = (uint32_t)sg[0].ctr[0];
+    c_drop = (uint32_t)sg[0].ctr[1];
+    c_late = (uint32_t)sg[0].ctr[2];
+    c_bat = (uint32_t)sg[0].ctr[3];
     c_busy = sg[0].ctr[4];
     g = 1;
     if (lazy_walk()) {  // joined everything: the true run ends at the last segment's end state
       t = sg[p.G - 1].t;
-      cursor = n;
+      cursor = ni;
     } else {
       materialize(sg + g - 1);
-      seg_end = g + 1 < p.G ? seg_begin(n, g + 1, p.G) : INT64_MAX;
+      seg_end = g + 1 < p.G ? (int32_t)seg_begin(n, g + 1, p.G) : INT32_MAX;
     }
   }
 
@@ -437,9 +442,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       ud = sd;
       ut = st;
     } else {
-      const int64_t idx = cursor + lane;
+      const int32_t idx = cursor + lane;
       ua = INT64_MAX;
-      if (idx < n) {
+      if (idx < ni) {
         ua = arr[idx];
         ud = dis[idx];
         ut = tbs[idx];
@@ -448,7 +453,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   };
   const int64_t a1 = p.prof.a[0], w1 = p.prof.w[0];
 
-  while (cursor < n || ncarry > 0) {
+  while (cursor < ni || ncarry > 0) {
     if constexpr (MODE == 1) {
       if (cursor >= seg_end) {  // first loop top past the segment: its end state, then the extension
         if (sm_ext.ld(0)) break;
@@ -462,7 +467,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
           sm_nrec.st(0, 0);
         }
         __syncwarp();
-        seg_end = seg_begin(n, g + 2, p.G);
+        seg_end = (int32_t)seg_begin(n, g + 2, p.G);
         // every extension iteration starts below s_{g+2}, which bounds the
         // scratch log (seg_log_off); a run already past it has no extension
         if (cursor >= seg_end) break;
@@ -478,7 +483,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
           if (lane < 7) reinterpret_cast<long long *>(ext ? &sg->ext[nr] : &sg->rec[nr])[lane] = v;
           int64_t m = rec_at - mb;
           while (m <= cursor - mb) m = seg_next_mark(m);
-          rec_at = nr + 1 < SEG_REC ? mb + m : INT64_MAX;
+          rec_at = nr + 1 < SEG_REC && mb + m < INT32_MAX ? (int32_t)(mb + m) : INT32_MAX;
           __syncwarp();
           if (lane == 0) sm_nrec.st(0, nr + 1);
           __syncwarp();
@@ -491,7 +496,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         ++crossed;
         ++g;
         nrec = 0;
-        seg_end = g + 1 < p.G ? seg_begin(n, g + 1, p.G) : INT64_MAX;
+        seg_end = g + 1 < p.G ? (int32_t)seg_begin(n, g + 1, p.G) : INT32_MAX;
         continue;
       }
       if (g < p.G && ncarry == 0) {
@@ -510,7 +515,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
               break;
             }
             materialize(sg + g - 1);
-            seg_end = g + 1 < p.G ? seg_begin(n, g + 1, p.G) : INT64_MAX;
+            seg_end = g + 1 < p.G ? (int32_t)seg_begin(n, g + 1, p.G) : INT32_MAX;
             continue;
           }
         }
@@ -627,9 +632,9 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const int nc = __popc(consumed);
       if (nc == 32) {  // whole lookahead consumed: reload all of it, scan on
         cursor += 32;
-        const int64_t idx = cursor + lane;
+        const int32_t idx = cursor + lane;
         ua = INT64_MAX;
-        if (idx < n) {
+        if (idx < ni) {
           ua = arr[idx];
           ud = dis[idx];
           ut = tbs[idx];
@@ -799,8 +804,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     const uint32_t mx = __reduce_max_sync(FULL, mem ? __float_as_uint(E) : 0u);
     kstar = (int)__reduce_min_sync(FULL, (mem && __float_as_uint(E) == mx) ? (uint32_t)lane : 32u) + 1;
     }
-    if (!ALG1) selm = kstar >= 32 ? FULL : ((1u << kstar) - 1u);
-    const bool sel = (selm >> lane) & 1u;
+    const bool sel = ALG1 ? ((selm >> lane) & 1u) != 0u : lane < kstar;
     const int mbin = (int)__reduce_max_sync(FULL, sel ? (uint32_t)tb : 0u);
     const int64_t dur = ALG1 ? (int64_t)__shfl_sync(FULL, my_ak, kstar - 1) +
                                    (int64_t)__shfl_sync(FULL, my_wk, kstar - 1) * mbin

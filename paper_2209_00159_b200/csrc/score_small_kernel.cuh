@@ -62,25 +62,26 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   const int K = (int)(n < kmax ? n : kmax);
   const int64_t now = p.now[q];
   const int32_t sig = lane < K ? sigma2(p.deadline[off + lane] - now) : 0;
-  const int idB = lane < K ? p.dist[off + lane] * B : 0;  // row offset of member lane's distribution
+  const int idB = lane < K ? p.dist[off + lane] * B * 4 : 0;  // byte offset of member lane's row
 
-  // a2: LG_k for k = 1..K, lanes over bins (bin lane + 32 e + 1)
+  // a2: LG_k for k = 1..K, lanes over bins (bin lane + 32 e + 1); 32-bit
+  // shared-space addresses (common.cuh SArr), kept in registers
   float acc[BPL];
 #pragma unroll
   for (int e = 0; e < BPL; ++e) acc[e] = 0.f;
   bool bok[BPL];
 #pragma unroll
   for (int e = 0; e < BPL; ++e) bok[e] = lane + 32 * e < B;
-  const float *s_lane = s_store + lane;
-  float *dst = lgs + 1 + lane;
-#pragma unroll 4
+  const uint32_t a_lane = smem_base(s_store) + 4u * lane;
+  const SArr<float> dst{opaque_u32(smem_addr(lgs) + 4u * (1 + lane))};
+#pragma unroll 8
   for (int k = 0; k < K; ++k) {
-    const float *src = s_lane + __shfl_sync(FULL, idB, k);
+    const uint32_t src = a_lane + (uint32_t)__shfl_sync(FULL, idB, k);
 #pragma unroll
     for (int e = 0; e < BPL; ++e) {
       if (bok[e]) {
-        acc[e] += src[32 * e];
-        dst[k * ROW + 32 * e] = acc[e];
+        acc[e] += lds_f32(src + 128u * e);
+        dst.st(k * ROW + 32 * e, acc[e]);
       }
     }
   }
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   // one broadcast 128-bit load); the butterfly sums over r.  Lanes >= K hold
   // sigma = 0, i.e. bin 0 and P = 0; rows k > K were not built, but they only
   // reach E_k for k > K, which is never used.
-  const uint32_t row0 = smem_addr(lgs);
+  const uint32_t row0 = opaque_u32(smem_addr(lgs));
   float pend[5];
   float E = 0.f;
 #pragma unroll

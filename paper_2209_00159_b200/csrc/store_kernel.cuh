@@ -163,7 +163,7 @@ __global__ void validate_trace_kernel(const int64_t *__restrict__ off, int64_t S
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t s = tid; s <= S; s += stride) {
     if (s == 0 && off[0] != 0) atomicOr(flags, 1u);
-    if (s > 0 && off[s] < off[s - 1]) atomicOr(flags, 1u);
+    if (s > 0 && (off[s] < off[s - 1] || off[s] - off[s - 1] > 0x7fffffbfll)) atomicOr(flags, 1u);
   }
   for (int64_t s = tid; s < S; s += stride) {
     if (slo[s] < 0 || bucket[s] < 0 || bucket[s] >= nb) atomicOr(flags, 1u);
