@@ -161,6 +161,13 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   return x;
 }
 __device__ __forceinline__ uint32_t smem_base(const void *p) { return opaque_u32(smem_addr(p)); }
+// a pointer the compiler must keep (or spill) rather than rebuild from thread / block ids in a loop
+template <class T>
+__device__ __forceinline__ T *opaque_ptr(T *p) {
+  uint64_t x = reinterpret_cast<uint64_t>(p);
+  asm volatile("mov.b64 %0, %1;" : "=l"(x) : "l"(x));
+  return reinterpret_cast<T *>(x);
+}
 
 template <class T> struct SArr;
 template <> struct SArr<int64_t> {

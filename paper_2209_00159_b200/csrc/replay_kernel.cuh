@@ -303,9 +303,16 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
     __syncwarp();
     if (g + 1 < p.G) seg_end = (int32_t)seg_begin(n, g + 1, p.G);
-    sg = p.seg + u;
+    sg = opaque_ptr(p.seg + u);  // used only in the (cold) segment hooks
     if (g > 0) mylog = p.seg_log ? p.seg_log + seg_log_off(base, s, n, g, p.G) : nullptr;
   }
+  // window slots start as valid entries (distribution 0, bin 1): the scoring
+  // reads every lane's slot and masks the non-members afterwards
+  w_dl.st(lane, 0);
+  w_h.st(lane, 0);
+  w_d.st(lane, 0);
+  w_tb.st(lane, 1);
+  __syncwarp();
   // lookahead: lane l holds arrivals[cursor + l] (arrival INT64_MAX beyond the trace)
   int64_t ua = INT64_MAX;
   int ud = 0, ut = 0;
@@ -411,7 +418,7 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   };
   if constexpr (MODE == 2) {
     // segment 0 ran from the true start: the true run is at its end state
-    sg = p.seg + s * p.G;
+    sg = opaque_ptr(p.seg + s * p.G);
     ndec = (int32_t)sg[0].ndec;  // segment 0 wrote its decisions into the true log
     taken = ndec;
     c_fin = (uint32_t)sg[0].ctr[0];
@@ -652,11 +659,13 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     if (wc == 0) continue;
 
     // ---- 2. score the window ---------------------------------------------
+    // window fields of every lane (slots >= wc hold stale entries: each use below
+    // is masked by mem / sel or indexes members only)
     const bool mem = lane < wc;
-    const int64_t Dr = mem ? w_dl.ld(lane) : 0;
-    const int32_t sig = mem ? sigma2(Dr - t) : 0;
-    const int dr = mem ? w_d.ld(lane) : 0;
-    const int tb = mem ? w_tb.ld(lane) : 0;
+    const int64_t Dr = w_dl.ld(lane);
+    const int32_t sig = sigma2(Dr - t);
+    const int dr = w_d.ld(lane);
+    const int tb = w_tb.ld(lane);
 
     int kstar = 1;  // a window of one has a single candidate: no scoring needed
     uint32_t selm = 1u;  // ALG1: the popped members (window positions)
@@ -716,15 +725,19 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
         if (j < pk) lgp += x;
       }
       const float pv = (bi > 0 && pk <= wc) ? ex2_approx(lgp) : 0.f;
-      float x[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        x[r] = 0.f;
-        if (r < PAIR_MAX && (r < 4 || wc > 4)) {  // warp-uniform
-          const float v = __shfl_sync(FULL, pv, (pq.z + r) & 31);
-          x[r] = r <= lane ? v : 0.f;
-        }
+      // gather through shared memory (the P matrix area, [k-1][8]): pair lane
+      // (k, r) writes P_r(k) to slot (k-1) 8 + r and a zero to the mirrored
+      // slot (7-k) 8 + 7-r, which no pair owns (r' = 7 - r >= k' = 8 - k): all
+      // 56 slots are rewritten every time, and lane k-1 reads its 8 as quads
+      if (lane < 28) {
+        Pm.st((pk - 1) * 8 + pq.y, pv);
+        Pm.st((7 - pk) * 8 + 7 - pq.y, 0.f);
       }
+      __syncwarp();
+      float x[8];
+      Pm.ldv<4>(8 * lane, *reinterpret_cast<float(*)[4]>(x));
+      if (wc > 4) Pm.ldv<4>(8 * lane + 4, *reinterpret_cast<float(*)[4]>(x + 4));  // warp-uniform
+      else x[4] = x[5] = x[6] = x[7] = 0.f;
       const float acc0 = (x[0] + x[1]) + (x[2] + x[3]);
       E = wc <= 4 ? acc0 : acc0 + ((x[4] + x[5]) + (x[6] + x[7]));
     } else {
