@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--replay-seg-sweep", action="store_true",
                     help="diagnostic: time the C5 sweep and its rank-0 shards for several segment counts")
     ap.add_argument("--no-shard-proxy", action="store_true")
+    ap.add_argument("--proxy-segments", default=None, help="segments per scenario in the shard proxy (default: as --replay-segments)")
     ap.add_argument("--no-policies", action="store_true", help="skip the replay policy-variant sweep")
     ap.add_argument("--policy-seeds", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
@@ -1113,7 +1114,7 @@ def shard_proxy(args, dev, ms_full):
             ts = []
             for _ in range(3):
                 sms, _, _ = time_replay(sf, 1, dev, lambda: None, lambda x: x, reduce=False,
-                                        segments=args.replay_segments)
+                                        segments=args.proxy_segments or args.replay_segments)
                 ts.append(sms)
             per_rank.append(float(np.median(ts)))
             segs = list(time_replay.segments)
