@@ -171,17 +171,87 @@ orloj_status alloc_flag(unsigned int **dflag, cudaStream_t s) {
   return ORLOJ_OK;
 }
 
-template <bool SMEM_TABLE, bool STEPS>
+// TIER 0's g polynomial (priority_kernel.cuh): P(u) ~ G(u) = e^{-b} (1 - e^{-b u/2}) / u
+// (G(0) = e^{-b} b / 2) on [0, U], the lowest degree D <= 5 that fits, by
+// interpolation at the D + 1 Chebyshev nodes (a Vandermonde solve in v = u / U, then c_k = q_k / U^k),
+// coefficients rounded to fp32.  Accepted when, on a grid of 257 points, the
+// fit holds to 2^-26 relative (fp64 coefficients) and to 2^-23 with the fp32
+// coefficients (each rounded once: 2^-24 of its term), and u P(u) stays far
+// from the fp32 range for every |u| <= 2^31 (j = 0 rows: g finite).
+bool prio_fit_g(double b, double U, float *c) {
+  constexpr int DMAX = 5;
+  auto G = [&](double u) { return u > 0.0 ? std::exp(-b) * -std::expm1(-b * u / 2.0) / u : std::exp(-b) * b / 2.0; };
+  // the lowest degree that fits (higher coefficients 0: no noise terms that
+  // would blow up outside [0, U])
+  for (int D = 0; D <= DMAX; ++D) {
+    double q[DMAX + 1] = {0.0};
+    if (U > 0.0 && D > 0) {
+      double A[DMAX + 1][DMAX + 2];
+      for (int i = 0; i <= D; ++i) {
+        const double v = 0.5 * (1.0 + std::cos(M_PI * (i + 0.5) / (D + 1)));
+        double pw = 1.0;
+        for (int k = 0; k <= D; ++k, pw *= v) A[i][k] = pw;
+        A[i][D + 1] = G(v * U);
+      }
+      for (int col = 0; col <= D; ++col) {  // Gauss-Jordan, partial pivoting
+        int piv = col;
+        for (int r = col + 1; r <= D; ++r)
+          if (std::fabs(A[r][col]) > std::fabs(A[piv][col])) piv = r;
+        for (int k = 0; k <= D + 1; ++k) std::swap(A[col][k], A[piv][k]);
+        for (int r = 0; r <= D; ++r) {
+          if (r == col) continue;
+          const double f = A[r][col] / A[col][col];
+          for (int k = col; k <= D + 1; ++k) A[r][k] -= f * A[col][k];
+        }
+      }
+      double sc = 1.0;
+      for (int k = 0; k <= D; ++k, sc /= U) q[k] = A[k][D + 1] / A[k][k] * sc;
+    } else {
+      q[0] = G(U / 2.0);
+    }
+    for (int k = 0; k <= DMAX; ++k) c[k] = (float)q[k];
+    auto P = [&](double u, bool f32) {
+      double r = f32 ? (double)c[DMAX] : q[DMAX];
+      for (int k = DMAX - 1; k >= 0; --k) r = r * u + (f32 ? (double)c[k] : q[k]);
+      return r;
+    };
+    bool ok = true;
+    for (int i = 0; i <= 256 && ok; ++i) {
+      const double u = U * i / 256.0;
+      ok = std::fabs(P(u, false) / G(u) - 1.0) <= std::ldexp(1.0, -26) &&  // the fit
+           std::fabs(P(u, true) / G(u) - 1.0) <= std::ldexp(1.0, -23);     // + fp32 coefficients
+    }
+    if (!ok) continue;
+    double bound = 0.0;  // bounds |u P(u)| and every Horner partial times u for |u| <= 2^31
+    for (int k = 0; k <= DMAX; ++k) bound += std::fabs((double)c[k]) * std::ldexp(1.0, 31 * (k + 1));
+    return bound < 1e37;
+  }
+  return false;
+}
+
+template <bool SMEM_TABLE, bool STEPS, int TIER>
 cudaError_t prio_launch(unsigned grid, size_t smem, cudaStream_t s, const double *log_table,
                         const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
-                        const StepsDev &steps, const orloj_queues *q, float *out) {
+                        const StepsDev &steps, const PrioCoef &cf, const orloj_queues *q, float *out,
+                        const float2 *gtab) {
   static std::atomic<uint64_t> configured{0};  // per instantiation and device
-  const cudaError_t e = ensure_max_dyn_smem(priority_scores_kernel<SMEM_TABLE, STEPS>, 96 << 10, configured);
+  const cudaError_t e = ensure_max_dyn_smem(priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 96 << 10, configured);
   if (e != cudaSuccess) return e;
-  priority_scores_kernel<SMEM_TABLE, STEPS><<<grid, 256, smem, s>>>(log_table, log_expected, S, B, b, prof, steps,
-                                                                    q->num_queues, q->queue_offsets,
-                                                                    q->deadline_ticks, q->now_ticks, out);
+  priority_scores_kernel<SMEM_TABLE, STEPS, TIER><<<grid, 256, smem, s>>>(
+      log_table, log_expected, S, B, b, prof, steps, cf, q->num_queues, q->queue_offsets, q->deadline_ticks,
+      q->now_ticks, out, gtab);
   return cudaGetLastError();
+}
+
+template <bool SMEM_TABLE, bool STEPS>
+cudaError_t prio_launch_tier(int tier, unsigned grid, size_t smem, cudaStream_t s, const double *log_table,
+                             const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
+                             const StepsDev &steps, const PrioCoef &cf, const orloj_queues *q, float *out,
+                             const float2 *gtab) {
+  return tier == 0 ? prio_launch<SMEM_TABLE, STEPS, 0>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
+                                                        cf, q, out, gtab)
+                   : prio_launch<SMEM_TABLE, STEPS, 1>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
+                                                        cf, q, out, gtab);
 }
 
 orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
@@ -219,20 +289,50 @@ orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_
   // Grid-stride over queues: ~resident blocks, so the per-size constants are
   // staged once per block, not once per 8 queues.
   const int B = store->num_bins;
-  const bool smem_table = PrioSmem::table_bytes(S, B) <= (64u << 10);
+  const bool smem_table = PrioSmem::table_bytes(S, B) <= (88u << 10);
   const size_t smem = PrioSmem::bytes(S, B, smem_table);
   const int64_t want = (queues->num_queues + 7) / 8;
   const int per_sm = smem <= (24u << 10) ? 8 : (int)((200u << 10) / smem);
   const int64_t cap = (int64_t)148 * (per_sm < 1 ? 1 : per_sm);
   const unsigned grid = (unsigned)(want < cap ? want : cap);
+  // Tier (priority_kernel.cuh): TIER 0 (strict-count lookup, fitted g) when
+  // the fit holds and every horizon a_k + w_k B + 1 fits under the tier's slack
+  // cap 2^30 - 2 - max w; else TIER 1.
+  int32_t wmax = 0;
+  for (int k = 0; k < S; ++k) wmax = prof.w[k] > wmax ? prof.w[k] : wmax;
+  const int64_t cap0 = (1ll << 30) - 2 - wmax;
+  PrioCoef cf;
+  bool t0 = b <= 0.05 && prio_fit_g(b, 2.0 * (wmax - 1), cf.c);
+  for (int k = 0; k < S && t0; ++k) t0 = (int64_t)prof.a[k] + (int64_t)prof.w[k] * B + 1 <= cap0;
+  const int tier = t0 ? 0 : 1;
+  cf.half_b = (float)(b / 2.0);
+  cf.gb = (float)(-std::expm1(-b));
+  cf.cap = t0 ? (int32_t)cap0 : 0x3fffffff;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
+  float2 *gtab = nullptr;
+  if (!smem_table) {
+    const int64_t ne = (int64_t)S * (B + 2);
+    if (cudaMallocAsync((void **)&gtab, (size_t)ne * sizeof(float2), s) != cudaSuccess)
+      return fail(ORLOJ_ERR_OOM, "priority_scores: cannot allocate the re-based table");
+    if (tier == 0)
+      priority_rebase_kernel<0><<<(unsigned)((ne + 255) / 256), 256, 0, s>>>(log_table, log_expected, S, B, b, prof,
+                                                                            gtab);
+    else
+      priority_rebase_kernel<1><<<(unsigned)((ne + 255) / 256), 256, 0, s>>>(log_table, log_expected, S, B, b, prof,
+                                                                            gtab);
+  }
   if (cs)
-    e = smem_table ? prio_launch<true, true>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out)
-                   : prio_launch<false, true>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out);
+    e = smem_table ? prio_launch_tier<true, true>(tier, grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
+                                                   cf, queues, out, gtab)
+                   : prio_launch_tier<false, true>(tier, grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
+                                                    cf, queues, out, gtab);
   else
-    e = smem_table ? prio_launch<true, false>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out)
-                   : prio_launch<false, false>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps, queues, out);
+    e = smem_table ? prio_launch_tier<true, false>(tier, grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
+                                                    cf, queues, out, gtab)
+                   : prio_launch_tier<false, false>(tier, grid, smem, s, log_table, log_expected, S, B, b, prof,
+                                                     steps, cf, queues, out, gtab);
+  if (gtab) cudaFreeAsync(gtab, s);
   if (e != cudaSuccess) return cuda_fail(e, "priority_scores launch");
   return ok();
 }

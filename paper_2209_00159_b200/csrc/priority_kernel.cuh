@@ -73,24 +73,50 @@ static __global__ void priority_table_kernel(const float *__restrict__ log2F, in
   logEL[bs - 1] = log(a + w * mean_bin);
 }
 
-// Warp per queue (grid-stride over queues: a block stages the per-size
-// constants once and reuses them for many queues), lanes over members, chunks
-// of 8 members per lane with the size loop outside the member loop (the
-// per-size constants are loaded once per 8 members).  Per block, shared memory
-// holds for every size k: the lookup constants {2a, 2wB, mag, sh} (one 16-B
-// load), w, and -- when SMEM_TABLE -- the table re-based on log E[L]:
-//   sC[k][i] = C[i] - log E[L]   (fp64: it meets b sigma, both can be large)
-//   sH[k][i] = H[i] - log E[L]   (fp32)
-// Per element (member r, size k), with A = sC[i*] - b sigma (fp64 -> fp32):
-//   no partial bin:  log p = A
-//   partial bin, x = sigma - l1 in (0, w):  g = 1 - e^{-b x},
-//      log p = log(e^A + e^{sH[i*+1]} g)  (prio_partial)
-// Output [S][N] (size-major: each store of a warp is one contiguous 128-B
-// line, and PopBatch reads one size row coalesced).
+// Score kernel (orloj_priority_scores).  Warp per queue (grid-stride over
+// queues: a block stages the per-size constants once and reuses them for many
+// queues), lanes over members, chunks of PRIO_CHUNK members per lane with the
+// size loop outside the member loop.  No fp64 and no branch per element: the
+// fp64 tables are re-based once per block into an fp32 table in shared memory
+// so that the full-bin term is one FFMA.
+//
+// TIER 1 (any b, any profile): entry (k, i), i = 0..B, is {C'_i, H'_{i+1}} with
+//   C'_i = C[i] - b l2_i - log E[L]   (l2_i = a_k + w_k i; -inf where C = -inf)
+//   H'_{i+1} = H[i+1] - log E[L]      (-inf at i = B: no bin beyond the last).
+// The scorer's lookup gives i = i*(sigma) and the exact integer x = sigma - l2_i:
+//   log p(full bins) = C[i] - b sigma - log E[L] = C'_i - b x,
+// and with x > 0, i < B (x is then sigma - l1_{i+1} in (0, w)) the partial bin
+//   log p = log(e^{lp} + e^{H'} g),  g = 1 - e^{-b x}   (prio_combine, general g).
+//
+// TIER 0 (when the host's polynomial fit below holds to 2^-25 and every
+// horizon a_k + w_k B + 1 is under the tier's slack cap; the P1 case): a
+// strict-count lookup
+//   j = #bins with l2 < sigma, + 1   (= floor((sigma - 1 - a + w) / w) clamped to [0, B+1])
+// puts sigma in bin j with x = sigma - l1_j in (0, w] for 1 <= j <= B (a full
+// last bin is the same value as a partial one at x = w), j = B+1 beyond the
+// last bin, and j = 0 exactly when sigma <= a (p = 0).  Entry (k, j), j = 0..B+1:
+//   {C[j-1] - b l1_j - b - log E[L],  H[j] - log E[L]},   entry 0 = {-inf, -inf},
+//   H'_{B+1} = -inf.
+// With u = 2 (x - 1) (an exact integer from the lookup, no select):
+//   lp = T.x - (b/2) u,   g = g_b + e_b g(b u / 2) = g_b + u P(u)
+// (g_b = 1 - e^{-b}, e_b = e^{-b}; both terms positive, no cancellation).  P is
+// a degree-5 polynomial fitted by the host (Chebyshev interpolation of
+// e_b (1 - e^{-b u/2}) / u on [0, 2 (max w - 1)], fp64, coefficients rounded
+// to fp32, then checked on a grid: 2^-26 relative for the fit, 2^-23 with the fp32 coefficients; else TIER 1).  j = 0
+// gives lp = Hn = -inf: prio_combine returns -inf (the host also checks that P
+// is finite for every u the cap allows).
+//
+// C' <= -log E[L] (each full-bin term is at most pm_j), so |C'| + b x = |log p|
+// whenever E[L] >= 1 tick: the fp32 re-based form keeps the 2^-23 relative
+// bound of an fp64 full-bin term.  Slack above the tier's cap (the
+// last entry there: the cap is above every profile's horizon) adds
+// b (sigma - cap) in a warp-uniform slow path.
+// Output [S][N] (size-major: each store of a warp is one contiguous 128-B line,
+// and PopBatch reads one size row coalesced).
 struct PrioSmem {
-  static __host__ __device__ size_t table_bytes(int S, int B) { return (size_t)S * (B + 1) * (8 + 4); }
+  static __host__ __device__ size_t table_bytes(int S, int B) { return (size_t)S * (B + 2) * 8; }
   static __host__ __device__ size_t bytes(int S, int B, bool smem_table) {
-    return (size_t)S * (16 + 4) + (smem_table ? table_bytes(S, B) : 0);
+    return (size_t)S * (16 + 8) + (smem_table ? table_bytes(S, B) : 0);
   }
 };
 
@@ -100,13 +126,10 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return y;
 }
 
-// The partial bin of Eq. 2 in the log domain: log(e^lp + e^Hn g), g = 1 - e^{-t},
-// t = b x > 0.  g: the Taylor series to t^8 below t = 1/2 (truncation < 2^-26
-// relative, no cancellation), else 1 - 2^{-t log2 e} (g > 0.39 there).  With
-// d = -|lp - Hn| one term of the sum is exactly 1:
-//   lp >= Hn:  lp + log(1 + e^d g),   else  Hn + log(e^d + g),
-// two MUFU (ex2, lg2) per element.
-__device__ __forceinline__ float prio_partial(float lp, float Hn, float t) {
+// g = 1 - e^{-t}, t = b x >= 0: the Taylor series to t^8 below t = 1/2
+// (truncation < 2^-26 relative, no cancellation), else 1 - 2^{-t log2 e}
+// (g > 0.39 there).  Both sides evaluated, one select (no divergence).
+__device__ __forceinline__ float prio_g_general(float t) {
   float c = -1.f / 40320.f;
   c = fmaf(c, t, 1.f / 5040.f);
   c = fmaf(c, t, -1.f / 720.f);
@@ -115,25 +138,39 @@ __device__ __forceinline__ float prio_partial(float lp, float Hn, float t) {
   c = fmaf(c, t, 1.f / 6.f);
   c = fmaf(c, t, -0.5f);
   c = fmaf(c, t, 1.f);
-  const float g = t < 0.5f ? c * t : 1.f - ex2_approx(-t * 1.4426950408889634f);
+  const float big = 1.f - ex2_approx(-t * 1.4426950408889634f);
+  return t < 0.5f ? c * t : big;
+}
+
+// The partial bin of Eq. 2 in the log domain: log(e^lp + e^Hn g).  With
+// d = -|lp - Hn| one term of the sum is exactly 1:
+//   lp >= Hn:  lp + log(1 + e^d g),   else  Hn + log(e^d + g),
+// two MUFU (ex2, lg2).  Hn = -inf (no partial bin) gives e = 0, y = 1 and lp
+// exactly; lp = Hn = -inf gives d = NaN, clamped to -150 (e = 0 after ftz),
+// and -inf.  g must be finite.
+__device__ __forceinline__ float prio_combine(float lp, float Hn, float g) {
+  const float e = ex2_approx(fmaxf(-fabsf(lp - Hn) * 1.4426950408889634f, -150.f));
   const bool hi = lp >= Hn;
-  const float e = ex2_approx(-fabsf(lp - Hn) * 1.4426950408889634f);
   const float y = hi ? fmaf(e, g, 1.f) : e + g;
   return fmaf(0.6931471805599453f, lg2_approx(y), hi ? lp : Hn);
 }
 
+// Pre-rebasing form kept for the replay's Alg. 1 PopBatch (replay_kernel.cuh),
+// which scores one window at a time from the fp64 global tables.
+__device__ __forceinline__ float prio_partial(float lp, float Hn, float t) {
+  return prio_combine(lp, Hn, prio_g_general(t));
+}
+
 // One element of the score kernel with the table read from global memory
-// (tab_k = table + (k-1) 2 (B+1)); the same arithmetic, value for value, as the
-// shared-memory path (which stages tab - lEL in fp64 and (float)(tab - lEL)).
+// (tab_k = table + (k-1) 2 (B+1)), fp64 full-bin term: the replay's Alg. 1 path.
 __device__ __forceinline__ float prio_elem_global(const double *__restrict__ tab_k, double lEL, int B, int4 lk,
                                                   int32_t w, int32_t s2, double bsig, float bf) {
   const int i = lookup_bin(s2, lk.x, lk.y, (uint32_t)lk.z, (uint32_t)lk.w);
   const int32_t x = ((s2 - lk.x) >> 1) - w * i;
   const double Ci = tab_k[i] - lEL;
   const float Hn = (i < B && x > 0) ? (float)(tab_k[B + 1 + i + 1] - lEL) : -INFINITY;
-  float lp = (float)(Ci + bsig);
-  if (Hn > -INFINITY) lp = prio_partial(lp, Hn, bf * (float)x);
-  return lp;
+  const float lp = (float)(Ci + bsig);
+  return prio_combine(lp, Hn, prio_g_general(bf * (float)(x > 0 ? x : 0)));
 }
 
 constexpr int PRIO_CHUNK = 8;  // members per lane per pass
@@ -148,100 +185,215 @@ struct StepsDev {
   double boff[PRIO_MAX_STEPS];   // b off[s]
 };
 
+// Per-call constants of the g tiers (host-computed in fp64, rounded once).
+struct PrioCoef {
+  float half_b;  // b / 2
+  float gb;      // 1 - e^{-b}
+  float c[6];    // P(u) = c0 + c1 u + ... + c5 u^5 (TIER 0, host-fitted)
+  int32_t cap;   // slack cap (ticks) of the tier's lookup
+};
+
 __device__ __forceinline__ float logaddexpf_(float a, float b) {
   const float M = fmaxf(a, b);
   return M == -INFINITY ? M : M + log1pf(__expf(fminf(a, b) - M));
 }
 
-template <bool SMEM_TABLE, bool STEPS>
+// Slack of a member, clamped to [0, cap] and doubled.
+__device__ __forceinline__ int32_t prio_s2(int64_t sigma, int32_t cap) {
+  return 2 * (int32_t)(sigma < 0 ? 0 : sigma > cap ? cap : sigma);
+}
+
+// Per-size constants in shared memory: lk = {lookup offset, 2 w (bins+1), mag,
+// sh}, nw2 = -2 w (TIER 0) or -w (TIER 1).
+template <int TIER>
+__device__ __forceinline__ int4 prio_lk(const ProfileDev &prof, int k, int B) {
+  return TIER == 0 ? make_int4(2 * (prof.a[k] + 1 - prof.w[k]), 2 * prof.w[k] * (B + 1), (int)prof.mag[k],
+                               (int)prof.sh[k])
+                   : make_int4(prof.a2[k], prof.wB2[k], (int)prof.mag[k], (int)prof.sh[k]);
+}
+
+// Re-based table entry (k, e) of the tier (layout above; stride B+2).
+template <int TIER>
+__device__ __forceinline__ float2 prio_entry(const double *__restrict__ table, const double *__restrict__ logEL,
+                                             const ProfileDev &prof, int B, double b, int k, int e) {
+  const double lEL = logEL[k];
+  const double *tab = table + (size_t)k * 2 * (B + 1);
+  const double a = prof.a[k], w = prof.w[k];
+  if (TIER == 0) {
+    if (e == 0) return make_float2(-INFINITY, -INFINITY);
+    const double C = tab[e - 1];
+    return make_float2(C == -INFINITY ? -INFINITY : (float)(C - b * (a + w * (e - 1)) - b - lEL),
+                       e <= B ? (float)(tab[B + 1 + e] - lEL) : -INFINITY);
+  }
+  if (e > B) return make_float2(-INFINITY, -INFINITY);  // unused pad
+  const double C = tab[e];
+  return make_float2(C == -INFINITY ? -INFINITY : (float)(C - b * (a + w * e) - lEL),
+                     e < B ? (float)(tab[B + 1 + e + 1] - lEL) : -INFINITY);
+}
+
+// Table row of one size: shared (a 32-bit shared-space address taken after the
+// staging barrier, so the non-volatile loads depend on it and stay below the
+// barrier) or global (tables above the shared-memory budget).
+struct PrioTabS {
+  uint32_t base;
+  __device__ __forceinline__ float2 ld(int j) const {
+    float2 v;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(base + 8u * (uint32_t)j));
+    return v;
+  }
+};
+struct PrioTabG {
+  const float2 *p;
+  __device__ __forceinline__ float2 ld(int j) const { return __ldg(p + j); }
+};
+
+// log p of one (member, size): s2 = prio_s2(sigma), tk the size's re-based
+// table row, bxe = b (sigma - cap) above the cap, else 0.
+template <int TIER, class Tab>
+__device__ __forceinline__ float prio_elem(const Tab &tk, const int4 &lk, int32_t nw, int32_t s2, float bf,
+                                           const PrioCoef &cf, float bxe) {
+  const int32_t x2 = s2 - lk.x;
+  int32_t xc = x2 < lk.y ? x2 : lk.y;
+  xc = xc > 0 ? xc : 0;
+  const int j = (int)(__umulhi((uint32_t)xc, (uint32_t)lk.z) >> (uint32_t)lk.w);
+  const float2 T = tk.ld(j);
+  if (TIER == 0) {
+    const float u = (float)(x2 + nw * j);  // 2 (x - 1), x = sigma - l1_j
+    const float lp = fmaf(-cf.half_b, u, T.x) - bxe;
+    float c = fmaf(cf.c[5], u, cf.c[4]);
+    c = fmaf(c, u, cf.c[3]);
+    c = fmaf(c, u, cf.c[2]);
+    c = fmaf(c, u, cf.c[1]);
+    c = fmaf(c, u, cf.c[0]);
+    return prio_combine(lp, T.y, fmaf(u, c, cf.gb));
+  } else {
+    const int32_t x = (x2 >> 1) + nw * j;  // sigma - l2_i
+    const float Hn = x > 0 ? T.y : -INFINITY;
+    const float xf = (float)x;
+    const float lp = fmaf(-bf, xf, T.x) - bxe;
+    return prio_combine(lp, Hn, prio_g_general(bf * fmaxf(xf, 0.f)));
+  }
+}
+
+// The size loop of one chunk (Tab: shared or global rows).
+template <int TIER, bool STEPS, class Tab>
+__device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const int4 *s_lk, const int2 *s_wk, int S,
+                                           float *out0, int64_t N, int nv, unsigned mode, const int64_t (&sg)[PRIO_CHUNK],
+                                           const int32_t (&s2)[PRIO_CHUNK], const float (&bxe)[PRIO_CHUNK],
+                                           double b, float bf, const PrioCoef &cf, const StepsDev &steps);
+
+template <bool SMEM_TABLE, bool STEPS, int TIER>
 __global__ void __launch_bounds__(256) priority_scores_kernel(
     const double *__restrict__ table, const double *__restrict__ logEL, int32_t S, int32_t B, double b,
-    const __grid_constant__ ProfileDev prof, const __grid_constant__ StepsDev steps, int64_t Q,
+    const __grid_constant__ ProfileDev prof, const __grid_constant__ StepsDev steps, const PrioCoef cf, int64_t Q,
     const int64_t *__restrict__ offsets, const int64_t *__restrict__ deadline, const int64_t *__restrict__ now,
-    float *__restrict__ out) {
+    float *__restrict__ out, const float2 *__restrict__ gtab) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int4 *s_lk = reinterpret_cast<int4 *>(smem_raw);                                          // [S]
-  double *s_C = reinterpret_cast<double *>(s_lk + S);                                       // [S][B+1]
-  float *s_H = reinterpret_cast<float *>(s_C + (SMEM_TABLE ? (size_t)S * (B + 1) : 0));    // [S][B+1]
-  int32_t *s_w = reinterpret_cast<int32_t *>(s_H + (SMEM_TABLE ? (size_t)S * (B + 1) : 0));  // [S]
+  int4 *s_lk = reinterpret_cast<int4 *>(smem_raw);       // [S]
+  int2 *s_wk = reinterpret_cast<int2 *>(s_lk + S);      // [S] {nw, unused}
+  float2 *s_T = reinterpret_cast<float2 *>(s_wk + S);   // [S][B+2] (SMEM_TABLE)
   for (int k = threadIdx.x; k < S; k += blockDim.x) {
-    s_lk[k] = make_int4(prof.a2[k], prof.wB2[k], (int)prof.mag[k], (int)prof.sh[k]);
-    s_w[k] = prof.w[k];
+    s_lk[k] = prio_lk<TIER>(prof, k, B);
+    s_wk[k] = make_int2(TIER == 0 ? -2 * prof.w[k] : -prof.w[k], 0);
   }
   if (SMEM_TABLE)
-    for (int e = threadIdx.x; e < S * (B + 1); e += blockDim.x) {
-      const int k = e / (B + 1), i = e - k * (B + 1);
-      const double lEL = logEL[k];
-      s_C[e] = table[(size_t)k * 2 * (B + 1) + i] - lEL;
-      s_H[e] = (float)(table[(size_t)k * 2 * (B + 1) + B + 1 + i] - lEL);
+    for (int e = threadIdx.x; e < S * (B + 2); e += blockDim.x) {
+      const int k = e / (B + 2);
+      s_T[e] = prio_entry<TIER>(table, logEL, prof, B, b, k, e - k * (B + 2));
     }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const float bf = (float)b;
   const int64_t base0 = offsets[0], N = offsets[Q] - base0;
   const int64_t wpb = blockDim.x >> 5;
-
-  // log p_single for size k at slack sigma (s2 = sigma2(sigma), bsig = -b sigma)
-  auto single = [&](int k, const int4 &lk, int32_t w, double lEL, int32_t s2, double bsig) -> float {
-    const int i = lookup_bin(s2, lk.x, lk.y, (uint32_t)lk.z, (uint32_t)lk.w);
-    // x = sigma - l1 of bin i+1 (exact: below the horizon 2 sigma - 2a fits int32;
-    // sigma < 0 gives x = -a <= 0)
-    const int32_t x = ((s2 - lk.x) >> 1) - w * i;
-    const bool part = i < B && x > 0;
-    double Ci;
-    float Hn = -INFINITY;
-    if (SMEM_TABLE) {
-      Ci = s_C[k * (B + 1) + i];
-      if (part) Hn = s_H[k * (B + 1) + i + 1];
-    } else {
-      Ci = table[(size_t)k * 2 * (B + 1) + i] - lEL;
-      if (part) Hn = (float)(table[(size_t)k * 2 * (B + 1) + B + 1 + i + 1] - lEL);
-    }
-    float lp = (float)(Ci + bsig);
-    if (Hn > -INFINITY) lp = prio_partial(lp, Hn, bf * (float)x);  // 0 < b x < b w
-    return lp;
-  };
+  const int32_t cap = cf.cap;
 
   for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < Q; q += (int64_t)gridDim.x * wpb) {
     const int64_t b0 = offsets[q] - base0, e0 = offsets[q + 1] - base0;
     const int64_t t = now[q];
     for (int64_t c0 = b0; c0 < e0; c0 += 32 * PRIO_CHUNK) {
-      // members of this lane in the chunk: c0 + lane + 32 m < e0  <=>  m < nv (32-bit compares below)
+      // members of this lane in the chunk: c0 + lane + 32 m < e0  <=>  m < nv
       const int64_t rem = e0 - c0 - lane;
       const int nv = rem <= 0 ? 0 : rem >= 32 * PRIO_CHUNK ? PRIO_CHUNK : (int)((rem + 31) >> 5);
-      double bsig[PRIO_CHUNK];  // -b sigma
       int64_t sg[PRIO_CHUNK];   // sigma (STEPS)
       int32_t s2[PRIO_CHUNK];
+      float bxe[PRIO_CHUNK];    // b (sigma - cap) above the cap
+      bool over = false;
 #pragma unroll
       for (int m = 0; m < PRIO_CHUNK; ++m) {
         const int64_t j = c0 + lane + 32 * m;
-        const int64_t sigma = j < e0 ? deadline[j] - t : 0;
+        const int64_t sigma = m < nv ? deadline[j] - t : 0;
         sg[m] = sigma;
-        bsig[m] = -b * (double)sigma;
-        s2[m] = sigma2(sigma);
+        s2[m] = prio_s2(sigma, cap);
+        bxe[m] = sigma > cap ? (float)(b * (double)(sigma - cap)) : 0.f;
+        over |= sigma > cap;
       }
-      for (int k = 0; k < S; ++k) {
-        const int4 lk = s_lk[k];
-        const int32_t w = s_w[k];
-        float *ok = out + (int64_t)k * N + c0 + lane;  // member m at ok[32 m]
-        const double lEL = SMEM_TABLE ? 0.0 : logEL[k];
-#pragma unroll
-        for (int m = 0; m < PRIO_CHUNK; ++m) {
-          if (m >= nv) break;
-          float lp;
-          if (STEPS) {
-            lp = -INFINITY;
-            for (int st = 0; st < steps.n; ++st)
-              lp = logaddexpf_(lp, steps.logdc[st] + single(k, lk, w, lEL, sigma2(sg[m] + steps.off[st]),
-                                                           bsig[m] - steps.boff[st]));
-          } else {
-            lp = single(k, lk, w, lEL, s2[m], bsig[m]);
-          }
-          ok[32 * m] = lp;
-        }
-      }
+      // warp-uniform specialisations: a full chunk stores unpredicated, and
+      // only a chunk with a slack above the cap pays the extra subtraction
+      const unsigned mode = (__any_sync(0xffffffffu, over) ? 1u : 0u) | (__all_sync(0xffffffffu, nv == PRIO_CHUNK) ? 2u : 0u);
+      float *out0 = out + c0 + lane;  // size k, member m at out0[k N + 32 m]
+      if (SMEM_TABLE)
+        prio_chunk<TIER, STEPS>(PrioTabS{smem_base(s_T)}, 8 * (B + 2), s_lk, s_wk, S, out0, N, nv, mode, sg, s2, bxe,
+                                b, bf, cf, steps);
+      else
+        prio_chunk<TIER, STEPS>(PrioTabG{gtab}, B + 2, s_lk, s_wk, S, out0, N, nv, mode, sg, s2, bxe, b, bf, cf, steps);
     }
   }
+}
+
+template <int TIER, bool STEPS, class Tab>
+__device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const int4 *s_lk, const int2 *s_wk, int S,
+                                           float *out0, int64_t N, int nv, unsigned mode, const int64_t (&sg)[PRIO_CHUNK],
+                                           const int32_t (&s2)[PRIO_CHUNK], const float (&bxe)[PRIO_CHUNK],
+                                           double b, float bf, const PrioCoef &cf, const StepsDev &steps) {
+  const int32_t cap = cf.cap;
+  Tab tk = t0;
+  for (int k = 0; k < S; ++k) {
+    const int4 lk = s_lk[k];
+    const int32_t nw = s_wk[k].x;
+    float *ok = out0 + (int64_t)k * N;  // member m at ok[32 m]
+    if (STEPS) {
+#pragma unroll 1
+      for (int m = 0; m < PRIO_CHUNK; ++m) {
+        float lp = -INFINITY;
+        for (int st = 0; st < steps.n; ++st) {
+          const int64_t sgs = sg[m] + steps.off[st];
+          const float bx = sgs > cap ? (float)(b * (double)(sgs - cap)) : 0.f;
+          lp = logaddexpf_(lp, steps.logdc[st] + prio_elem<TIER>(tk, lk, nw, prio_s2(sgs, cap), bf, cf, bx));
+        }
+        if (m < nv) ok[32 * m] = lp;
+      }
+    } else if (mode == 2u) {
+#pragma unroll
+      for (int m = 0; m < PRIO_CHUNK; ++m) ok[32 * m] = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, 0.f);
+    } else if (mode == 0u) {
+#pragma unroll
+      for (int m = 0; m < PRIO_CHUNK; ++m) {
+        const float lp = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, 0.f);
+        if (m < nv) ok[32 * m] = lp;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < PRIO_CHUNK; ++m) {
+        const float lp = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, bxe[m]);
+        if (m < nv) ok[32 * m] = lp;
+      }
+    }
+    if constexpr (sizeof(Tab) == sizeof(uint32_t)) tk.base += (uint32_t)rowb;
+    else tk.p += rowb;
+  }
+}
+
+// Re-based table in global memory (sizes whose table exceeds the shared-memory
+// budget): one thread per entry, the same values as the shared-memory staging.
+template <int TIER>
+__global__ void priority_rebase_kernel(const double *__restrict__ table, const double *__restrict__ logEL, int32_t S,
+                                       int32_t B, double b, const __grid_constant__ ProfileDev prof,
+                                       float2 *__restrict__ gtab) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)S * (B + 2)) return;
+  const int k = (int)(e / (B + 2));
+  gtab[e] = prio_entry<TIER>(table, logEL, prof, B, b, k, (int)(e - (int64_t)k * (B + 2)));
 }
 
 // Compare-exchange for a descending sort of (key, -index) pairs: after it,
@@ -260,14 +412,43 @@ __device__ __forceinline__ void cx(uint32_t &ka, int &ia, uint32_t &kb, int &ib)
 // log-priority for batch size bs, ties -> earlier member; -inf (no bin of L_bs
 // fits before the deadline) and NaN are never selected.  Writes member indices
 // (relative to the queue, highest priority first) to sel[q][0..bs), -1 after
-// the last.  Warp per queue, members strided over lanes, 8 per lane (n <= 256):
-// each lane sorts its 8 once (19-comparator network), then every round the
-// lane holding the best head (REDUX max over keys, then min over member
-// indices among equal keys) pops it.  Round r's winner is kept by lane r and
-// the 32 results leave in one coalesced store.
+// the last.  Warp per queue, member r = 32 s + lane in lane `lane`, slot s
+// (n <= 256), keys order-preserving (0 = not selectable).
+//
+// Fast path (exact, warp-uniform test): let each lane's head be its best member
+// (first of its maximal keys) and k2 its best other key.  If min over lanes of
+// the head keys > max over lanes of k2, every one of the top 32 is a head (32
+// heads beat every other member), so the answer is the 32 heads in order: one
+// bitonic sort of (key desc, index asc) across the lanes, rank r ends in lane
+// r, and lane r writes its member when r < bs.  A queue whose top 32 form a
+// contiguous run of members (a unimodal priority over the deadline-sorted
+// queue) always takes it.
+// General path: each lane sorts its 8 (19-comparator network), keeps its head in
+// registers and the rest in shared memory; every round the lane holding the
+// best head (REDUX max over keys, then min over member indices among equal
+// keys) pops it and loads its next; round r's winner is kept by lane r.
+__device__ __forceinline__ void pop_bitonic32(uint32_t &key, int &id, int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      const uint32_t pk = __shfl_xor_sync(FULL, key, j);
+      const int pid = __shfl_xor_sync(FULL, id, j);
+      const bool pbetter = pk > key || (pk == key && pid < id);
+      // in a descending block the lower lane of a pair keeps the better one
+      const bool keep_better = ((lane & j) == 0) == ((lane & kk) == 0);
+      const bool take = keep_better == pbetter;
+      key = take ? pk : key;
+      id = take ? pid : id;
+    }
+  }
+}
+
 static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__restrict__ logp, int32_t S, int64_t Q,
-                                                        const int64_t *__restrict__ offsets,
-                                                        const int32_t *__restrict__ bs_q, int32_t *__restrict__ sel) {
+                                                               const int64_t *__restrict__ offsets,
+                                                               const int32_t *__restrict__ bs_q,
+                                                               int32_t *__restrict__ sel) {
+  __shared__ uint2 s_list[8][9][32];  // per warp: sorted (key, id) positions 1..7 of each lane, 8 = sentinel
   const int lane = threadIdx.x & 31;
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (q >= Q) return;
@@ -277,17 +458,36 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
   int bs = bs_q[q];
   bs = (bs >= 1 && bs <= S) ? bs : 0;
   uint32_t k[8];
-  int id[8];
+  const float *row = logp + (int64_t)(bs ? bs - 1 : 0) * N + b0;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const int r = 32 * s + lane;
-    id[s] = r;
     k[s] = 0u;
     if (r < n && bs) {
-      const float v = logp[(int64_t)(bs - 1) * N + b0 + r];
-      k[s] = (v == -INFINITY || v != v) ? 0u : fkey(v == 0.0f ? 0.0f : v);  // -0 ties +0
+      const float v = row[r];
+      k[s] = (v == -INFINITY || v != v) ? 0u : fkey(v + 0.0f);  // -0 + 0 = +0: -0 ties +0
     }
   }
+  // lane head (first maximal slot) and the best other key
+  uint32_t kh = k[0], k2 = 0u;
+  int sh = 0;
+#pragma unroll
+  for (int s = 1; s < 8; ++s) {
+    const bool gt = k[s] > kh;
+    k2 = gt ? kh : max(k2, k[s]);
+    sh = gt ? s : sh;
+    kh = gt ? k[s] : kh;
+  }
+  if (__reduce_min_sync(FULL, kh) > __reduce_max_sync(FULL, k2)) {
+    uint32_t key = kh;
+    int id = 32 * sh + lane;
+    pop_bitonic32(key, id, lane);
+    sel[q * 32 + lane] = lane < bs ? id : -1;
+    return;
+  }
+  int id[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) id[s] = 32 * s + lane;
   // Batcher odd-even merge sort network for 8 (19 comparators), descending.
   cx(k[0], id[0], k[1], id[1]); cx(k[2], id[2], k[3], id[3]); cx(k[4], id[4], k[5], id[5]); cx(k[6], id[6], k[7], id[7]);
   cx(k[0], id[0], k[2], id[2]); cx(k[1], id[1], k[3], id[3]); cx(k[4], id[4], k[6], id[6]); cx(k[5], id[5], k[7], id[7]);
@@ -295,19 +495,23 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
   cx(k[0], id[0], k[4], id[4]); cx(k[1], id[1], k[5], id[5]); cx(k[2], id[2], k[6], id[6]); cx(k[3], id[3], k[7], id[7]);
   cx(k[2], id[2], k[4], id[4]); cx(k[3], id[3], k[5], id[5]);
   cx(k[1], id[1], k[2], id[2]); cx(k[3], id[3], k[4], id[4]); cx(k[5], id[5], k[6], id[6]);
-  int mine = -1;
-  for (int round = 0; round < bs; ++round) {
-    const uint32_t mx = __reduce_max_sync(FULL, k[0]);
-    if (mx == 0u) break;  // no selectable member left (warp-uniform)
-    const int win = (int)__reduce_min_sync(FULL, k[0] == mx ? (uint32_t)id[0] : 0x7fffffffu);
-    if (lane == round) mine = win;
-    if (id[0] == win && k[0] == mx) {  // pop the head
+  uint2(*lst)[32] = s_list[threadIdx.x >> 5];
 #pragma unroll
-      for (int s = 0; s < 7; ++s) {
-        k[s] = k[s + 1];
-        id[s] = id[s + 1];
-      }
-      k[7] = 0u;
+  for (int s = 1; s < 8; ++s) lst[s][lane] = make_uint2(k[s], (uint32_t)id[s]);
+  lst[8][lane] = make_uint2(0u, 0x7fffffffu);
+  __syncwarp();
+  uint32_t hk = k[0];
+  int hid = id[0], pos = 0, mine = -1;
+  for (int round = 0; round < bs; ++round) {
+    const uint32_t mx = __reduce_max_sync(FULL, hk);
+    if (mx == 0u) break;  // no selectable member left (warp-uniform)
+    const int win = (int)__reduce_min_sync(FULL, hk == mx ? (uint32_t)hid : 0x7fffffffu);
+    if (lane == round) mine = win;
+    if (hid == win) {  // pop the head (member indices are distinct)
+      pos = pos < 8 ? pos + 1 : 8;
+      const uint2 nx = lst[pos][lane];
+      hk = nx.x;
+      hid = (int)nx.y;
     }
   }
   sel[q * 32 + lane] = mine;

@@ -247,3 +247,66 @@ def test_piecewise_step_scores_vs_oracle(name):
     for bad in (([0, 0], [1.0, 2.0]), ([0, 5], [1.0, 1.0]), ([0], [0.0]), (list(range(9)), [float(i + 1) for i in range(9)])):
         with pytest.raises(orj.OrlojError):
             tab.scores(qs, steps=bad)
+
+
+def _fast_path_queues(off, v, bs):
+    """Queues on PopBatch's fast path (priority_kernel.cuh): min over lanes of
+    the lane-best key > max over lanes of every other key (order-preserving
+    keys, -inf / NaN / bs out of range -> not selectable).  Host restatement of
+    the kernel's warp-uniform test, used only to show both paths ran."""
+    fast = np.zeros(len(bs), bool)
+    for qi in range(len(bs)):
+        b = int(bs[qi])
+        n = int(off[qi + 1] - off[qi])
+        if not 1 <= b <= S or n < 32:
+            continue
+        x = np.full(256, -np.inf)
+        x[:min(n, 256)] = v[off[qi]:off[qi] + min(n, 256), b - 1]
+        x[~np.isfinite(x) & ~(x > 0)] = -np.inf  # -inf / NaN: not selectable
+        lanes = x.reshape(8, 32)  # slot s, lane l: member 32 s + l
+        head = lanes.max(axis=0)
+        other = np.sort(lanes, axis=0)[-2]
+        fast[qi] = np.isfinite(head).all() and head.min() > other.max()
+    return fast
+
+
+def test_pop_batch_fast_and_general_paths_bitexact():
+    """PopBatch on queues whose priorities are unimodal over the member index
+    (the top 32 a contiguous run: one head per lane, the fast path), with
+    exact ties planted at the lane heads (equal keys ordered by member index),
+    with a tie between a head and a second member (general path), and queues
+    shorter than 32 (general path).  Bit-exact against the oracle."""
+    rng = np.random.default_rng(gen.SEED_BASE + 930)
+    Q = 400
+    lengths = rng.integers(32, 257, Q)
+    lengths[:6] = (32, 256, 256, 31, 5, 256)
+    off = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    N = int(off[-1])
+    v = np.empty((N, S), np.float32)
+    for qi in range(Q):
+        n = int(lengths[qi])
+        r = np.arange(n)
+        for s in range(S):
+            peak = rng.uniform(0, n)
+            v[off[qi]:off[qi + 1], s] = (-np.abs(r - peak) * rng.uniform(0.01, 0.5)).astype(np.float32)
+    v[off[1]:off[2], :] = np.float32(-1.0)                   # 256 equal keys: each head ties its lane's next
+    v[off[2]:off[2] + 32, :] = np.float32(-0.5)              # 32 equal heads, everything else lower
+    v[off[2] + 32:off[3], :] = np.float32(-0.75)
+    bs = rng.integers(1, S + 1, Q).astype(np.int32)
+    bs[:6] = (32, 32, 32, 32, 3, 17)
+    q = orj.Queues.from_numpy(off, np.zeros(N), np.zeros(N), np.zeros(Q))
+    fam = gen.gpt_family(gen.SEED_BASE + 915)
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    prof = gen.eq3_half(fam, S)
+    tab = orj.PriorityTable(store, orj.LatencyProfile(prof.a, prof.w), S, 1e-4)
+    sel = tab.pop(q, torch.from_numpy(np.ascontiguousarray(v.T)).cuda(), torch.from_numpy(bs).cuda()).cpu().numpy()
+    for qi in range(Q):
+        want = pr.pop_batch(v[off[qi]:off[qi + 1]], int(bs[qi]), S)
+        got = [int(x) for x in sel[qi] if x >= 0]
+        assert got == want, qi
+        assert (sel[qi, len(got):] == -1).all()
+    fast = _fast_path_queues(off, v, bs)
+    assert fast[2] and not fast[1] and not fast[3] and not fast[4]
+    assert 0.3 < fast.mean() < 1.0, fast.mean()
+    import _parity as par
+    par.record("pop_batch_paths", label="unimodal+ties", queues=Q, fast_path=int(fast.sum()))
