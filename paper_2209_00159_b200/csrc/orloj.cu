@@ -235,8 +235,18 @@ cudaError_t prio_launch(unsigned grid, size_t smem, cudaStream_t s, const double
                         const StepsDev &steps, const PrioCoef &cf, const orloj_queues *q, float *out,
                         const float2 *gtab) {
   static std::atomic<uint64_t> configured{0};  // per instantiation and device
-  const cudaError_t e = ensure_max_dyn_smem(priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 96 << 10, configured);
+  cudaError_t e = ensure_max_dyn_smem(priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 96 << 10, configured);
   if (e != cudaSuccess) return e;
+  // one wave of resident blocks (grid-stride over queues): the per-size tables
+  // are staged once per block
+  int dev = 0, sms = 148, occ = 1;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 256,
+                                                         smem)) != cudaSuccess)
+    return e;
+  const int64_t cap = (int64_t)sms * (occ < 1 ? 1 : occ);
+  grid = (unsigned)((int64_t)grid < cap ? grid : cap);
   priority_scores_kernel<SMEM_TABLE, STEPS, TIER><<<grid, 256, smem, s>>>(
       log_table, log_expected, S, B, b, prof, steps, cf, q->num_queues, q->queue_offsets, q->deadline_ticks,
       q->now_ticks, out, gtab);
@@ -292,9 +302,7 @@ orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_
   const bool smem_table = PrioSmem::table_bytes(S, B) <= (88u << 10);
   const size_t smem = PrioSmem::bytes(S, B, smem_table);
   const int64_t want = (queues->num_queues + 7) / 8;
-  const int per_sm = smem <= (24u << 10) ? 8 : (int)((200u << 10) / smem);
-  const int64_t cap = (int64_t)148 * (per_sm < 1 ? 1 : per_sm);
-  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  const unsigned grid = (unsigned)(want < (1 << 30) ? want : (1 << 30));  // capped at one wave in prio_launch
   // Tier (priority_kernel.cuh): TIER 0 (strict-count lookup, fitted g) when
   // the fit holds and every horizon a_k + w_k B + 1 fits under the tier's slack
   // cap 2^30 - 2 - max w; else TIER 1.

@@ -174,6 +174,9 @@ __device__ __forceinline__ float prio_elem_global(const double *__restrict__ tab
 }
 
 constexpr int PRIO_CHUNK = 8;  // members per lane per pass
+#ifndef PRIO_MIN_BLOCKS
+#define PRIO_MIN_BLOCKS  // experiments: -DPRIO_MIN_BLOCKS=,5 caps registers for 5 resident blocks per SM
+#endif
 constexpr int PRIO_MAX_STEPS = 8;
 
 // Piecewise-step cost: deadlines D_r + off[s] with cost
@@ -283,7 +286,7 @@ __device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const in
                                            double b, float bf, const PrioCoef &cf, const StepsDev &steps);
 
 template <bool SMEM_TABLE, bool STEPS, int TIER>
-__global__ void __launch_bounds__(256) priority_scores_kernel(
+__global__ void __launch_bounds__(256 PRIO_MIN_BLOCKS) priority_scores_kernel(
     const double *__restrict__ table, const double *__restrict__ logEL, int32_t S, int32_t B, double b,
     const __grid_constant__ ProfileDev prof, const __grid_constant__ StepsDev steps, const PrioCoef cf, int64_t Q,
     const int64_t *__restrict__ offsets, const int64_t *__restrict__ deadline, const int64_t *__restrict__ now,
@@ -307,37 +310,85 @@ __global__ void __launch_bounds__(256) priority_scores_kernel(
   const int64_t base0 = offsets[0], N = offsets[Q] - base0;
   const int64_t wpb = blockDim.x >> 5;
   const int32_t cap = cf.cap;
+  const bool vec_ok = (N & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(deadline) & 15) == 0;
 
   for (int64_t q = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); q < Q; q += (int64_t)gridDim.x * wpb) {
     const int64_t b0 = offsets[q] - base0, e0 = offsets[q + 1] - base0;
     const int64_t t = now[q];
     for (int64_t c0 = b0; c0 < e0; c0 += 32 * PRIO_CHUNK) {
-      // members of this lane in the chunk: c0 + lane + 32 m < e0  <=>  m < nv
+      // Member of (lane, m): the strided map c0 + lane + 32 m, or (a full chunk
+      // at a 4-aligned start, aligned arrays) the vector map c0 + 128 (m / 4) +
+      // 4 lane + m % 4: each lane loads 4 consecutive deadlines (2 x 16 B) and
+      // stores 4 consecutive scores (16 B) per size.
+      const bool vec = vec_ok && e0 - c0 >= 32 * PRIO_CHUNK && (c0 & 3) == 0;  // warp-uniform
       const int64_t rem = e0 - c0 - lane;
-      const int nv = rem <= 0 ? 0 : rem >= 32 * PRIO_CHUNK ? PRIO_CHUNK : (int)((rem + 31) >> 5);
-      int64_t sg[PRIO_CHUNK];   // sigma (STEPS)
+      const int nv = vec ? PRIO_CHUNK : rem <= 0 ? 0 : rem >= 32 * PRIO_CHUNK ? PRIO_CHUNK : (int)((rem + 31) >> 5);
+      int64_t sg[PRIO_CHUNK];   // sigma
       int32_t s2[PRIO_CHUNK];
-      float bxe[PRIO_CHUNK];    // b (sigma - cap) above the cap
+      float bxe[PRIO_CHUNK];    // b (sigma - cap) above the cap, else 0
       bool over = false;
+      // all loads first, unconditional (a lane past the queue end re-reads the
+      // last member: in bounds, never stored), so they are in flight together
+      int64_t dl[PRIO_CHUNK];
+      if (vec) {
+#pragma unroll
+        for (int h = 0; h < PRIO_CHUNK / 4; ++h) {
+          const longlong2 *p2 = reinterpret_cast<const longlong2 *>(deadline + c0 + 128 * h + 4 * lane);
+          const longlong2 x0 = __ldg(p2), x1 = __ldg(p2 + 1);
+          dl[4 * h] = x0.x;
+          dl[4 * h + 1] = x0.y;
+          dl[4 * h + 2] = x1.x;
+          dl[4 * h + 3] = x1.y;
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < PRIO_CHUNK; ++m) {
+          const int64_t j = c0 + lane + 32 * m;
+          dl[m] = __ldg(deadline + (j < e0 ? j : e0 - 1));
+        }
+      }
 #pragma unroll
       for (int m = 0; m < PRIO_CHUNK; ++m) {
-        const int64_t j = c0 + lane + 32 * m;
-        const int64_t sigma = m < nv ? deadline[j] - t : 0;
+        const int64_t sigma = m < nv ? dl[m] - t : 0;
         sg[m] = sigma;
         s2[m] = prio_s2(sigma, cap);
-        bxe[m] = sigma > cap ? (float)(b * (double)(sigma - cap)) : 0.f;
         over |= sigma > cap;
       }
-      // warp-uniform specialisations: a full chunk stores unpredicated, and
-      // only a chunk with a slack above the cap pays the extra subtraction
-      const unsigned mode = (__any_sync(0xffffffffu, over) ? 1u : 0u) | (__all_sync(0xffffffffu, nv == PRIO_CHUNK) ? 2u : 0u);
-      float *out0 = out + c0 + lane;  // size k, member m at out0[k N + 32 m]
+      over = __any_sync(0xffffffffu, over);
+#pragma unroll
+      for (int m = 0; m < PRIO_CHUNK; ++m) bxe[m] = over && sg[m] > cap ? (float)(b * (double)(sg[m] - cap)) : 0.f;
+      // warp-uniform specialisations: a full chunk stores unpredicated, the
+      // vector map stores 16 B, and only a chunk with a slack above the cap
+      // pays the extra subtraction
+      const unsigned mode = (over ? 1u : 0u) | (__all_sync(0xffffffffu, nv == PRIO_CHUNK) ? 2u : 0u) | (vec ? 4u : 0u);
+      float *out0 = out + c0 + (vec ? 4 * lane : lane);
       if (SMEM_TABLE)
         prio_chunk<TIER, STEPS>(PrioTabS{smem_base(s_T)}, 8 * (B + 2), s_lk, s_wk, S, out0, N, nv, mode, sg, s2, bxe,
                                 b, bf, cf, steps);
       else
         prio_chunk<TIER, STEPS>(PrioTabG{gtab}, B + 2, s_lk, s_wk, S, out0, N, nv, mode, sg, s2, bxe, b, bf, cf, steps);
     }
+  }
+}
+
+// One size's scores of a chunk: PRED stores only members m < nv; VEC stores
+// groups of 4 consecutive members as one 16-B store (out at ok + 128 (m / 4)).
+template <int TIER, bool PRED, bool OVER, bool VEC, class Tab>
+__device__ __forceinline__ void prio_size(const Tab &tk, const int4 &lk, int32_t nw, float *ok, int nv,
+                                          const int32_t (&s2)[PRIO_CHUNK], const float (&bxe)[PRIO_CHUNK], float bf,
+                                          const PrioCoef &cf) {
+  float r[PRIO_CHUNK];
+#pragma unroll
+  for (int m = 0; m < PRIO_CHUNK; ++m) r[m] = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, OVER ? bxe[m] : 0.f);
+  if (VEC) {
+#pragma unroll
+    for (int h = 0; h < PRIO_CHUNK / 4; ++h)
+      *reinterpret_cast<float4 *>(ok + 128 * h) = make_float4(r[4 * h], r[4 * h + 1], r[4 * h + 2], r[4 * h + 3]);
+  } else {
+#pragma unroll
+    for (int m = 0; m < PRIO_CHUNK; ++m)
+      if (!PRED || m < nv) ok[32 * m] = r[m];
   }
 }
 
@@ -348,11 +399,15 @@ __device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const in
                                            double b, float bf, const PrioCoef &cf, const StepsDev &steps) {
   const int32_t cap = cf.cap;
   Tab tk = t0;
-  for (int k = 0; k < S; ++k) {
-    const int4 lk = s_lk[k];
-    const int32_t nw = s_wk[k].x;
-    float *ok = out0 + (int64_t)k * N;  // member m at ok[32 m]
-    if (STEPS) {
+  auto step = [&]() {
+    if constexpr (sizeof(Tab) == sizeof(uint32_t)) tk.base += (uint32_t)rowb;
+    else tk.p += rowb;
+  };
+  if (STEPS) {
+    for (int k = 0; k < S; ++k, step()) {
+      const int4 lk = s_lk[k];
+      const int32_t nw = s_wk[k].x;
+      float *ok = out0 + (int64_t)k * N;
 #pragma unroll 1
       for (int m = 0; m < PRIO_CHUNK; ++m) {
         float lp = -INFINITY;
@@ -361,26 +416,36 @@ __device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const in
           const float bx = sgs > cap ? (float)(b * (double)(sgs - cap)) : 0.f;
           lp = logaddexpf_(lp, steps.logdc[st] + prio_elem<TIER>(tk, lk, nw, prio_s2(sgs, cap), bf, cf, bx));
         }
-        if (m < nv) ok[32 * m] = lp;
-      }
-    } else if (mode == 2u) {
-#pragma unroll
-      for (int m = 0; m < PRIO_CHUNK; ++m) ok[32 * m] = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, 0.f);
-    } else if (mode == 0u) {
-#pragma unroll
-      for (int m = 0; m < PRIO_CHUNK; ++m) {
-        const float lp = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, 0.f);
-        if (m < nv) ok[32 * m] = lp;
-      }
-    } else {
-#pragma unroll
-      for (int m = 0; m < PRIO_CHUNK; ++m) {
-        const float lp = prio_elem<TIER>(tk, lk, nw, s2[m], bf, cf, bxe[m]);
-        if (m < nv) ok[32 * m] = lp;
+        if (m < nv) ok[(mode & 4u) ? 128 * (m >> 2) + (m & 3) : 32 * m] = lp;
       }
     }
-    if constexpr (sizeof(Tab) == sizeof(uint32_t)) tk.base += (uint32_t)rowb;
-    else tk.p += rowb;
+    return;
+  }
+  if (mode == 6u) {  // the common case: full, vector, no slack above the cap; two sizes per iteration
+    int k = 0;
+    for (; k + 1 < S; k += 2) {
+      const int4 lk0 = s_lk[k], lk1 = s_lk[k + 1];
+      const int32_t nw0 = s_wk[k].x, nw1 = s_wk[k + 1].x;
+      float *ok = out0 + (int64_t)k * N;
+      prio_size<TIER, false, false, true>(tk, lk0, nw0, ok, nv, s2, bxe, bf, cf);
+      step();
+      prio_size<TIER, false, false, true>(tk, lk1, nw1, ok + N, nv, s2, bxe, bf, cf);
+      step();
+    }
+    if (k < S) prio_size<TIER, false, false, true>(tk, s_lk[k], s_wk[k].x, out0 + (int64_t)k * N, nv, s2, bxe, bf, cf);
+    return;
+  }
+  for (int k = 0; k < S; ++k, step()) {
+    const int4 lk = s_lk[k];
+    const int32_t nw = s_wk[k].x;
+    float *ok = out0 + (int64_t)k * N;
+    switch (mode) {
+      case 7u: prio_size<TIER, false, true, true>(tk, lk, nw, ok, nv, s2, bxe, bf, cf); break;
+      case 2u: prio_size<TIER, false, false, false>(tk, lk, nw, ok, nv, s2, bxe, bf, cf); break;
+      case 3u: prio_size<TIER, false, true, false>(tk, lk, nw, ok, nv, s2, bxe, bf, cf); break;
+      case 0u: prio_size<TIER, true, false, false>(tk, lk, nw, ok, nv, s2, bxe, bf, cf); break;
+      default: prio_size<TIER, true, true, false>(tk, lk, nw, ok, nv, s2, bxe, bf, cf); break;
+    }
   }
 }
 
@@ -416,33 +481,40 @@ __device__ __forceinline__ void cx(uint32_t &ka, int &ia, uint32_t &kb, int &ib)
 // (n <= 256), keys order-preserving (0 = not selectable).
 //
 // Fast path (exact, warp-uniform test): let each lane's head be its best member
-// (first of its maximal keys) and k2 its best other key.  If min over lanes of
-// the head keys > max over lanes of k2, every one of the top 32 is a head (32
-// heads beat every other member), so the answer is the 32 heads in order: one
+// (first of its maximal keys) and k2 its best other key.  If every k2 is below
+// every selectable head, the selectable members in order are the selectable
+// heads, then (if any) selectable non-heads; so when either no non-head is
+// selectable or at least bs heads are, the answer is the best bs heads: one
 // bitonic sort of (key desc, index asc) across the lanes, rank r ends in lane
-// r, and lane r writes its member when r < bs.  A queue whose top 32 form a
-// contiguous run of members (a unimodal priority over the deadline-sorted
-// queue) always takes it.
+// r, and lane r writes its member when r < bs and it is selectable.  A queue
+// whose selectable top forms a contiguous run of at most 32 members (e.g. a
+// unimodal priority over the deadline-sorted queue, or the few members with
+// enough slack for a large batch) always takes it.
 // General path: each lane sorts its 8 (19-comparator network), keeps its head in
 // registers and the rest in shared memory; every round the lane holding the
 // best head (REDUX max over keys, then min over member indices among equal
 // keys) pops it and loads its next; round r's winner is kept by lane r.
-__device__ __forceinline__ void pop_bitonic32(uint32_t &key, int &id, int lane) {
+// Bitonic sort of one packed (key << 32 | ~member) per lane across the warp,
+// descending: rank r ends in lane r.  Packed keys are distinct (distinct
+// members), so one 64-bit compare orders (key desc, member asc).
+__device__ __forceinline__ uint64_t pop_bitonic32(uint64_t me, int lane) {
 #pragma unroll
   for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll
     for (int j = kk >> 1; j > 0; j >>= 1) {
-      const uint32_t pk = __shfl_xor_sync(FULL, key, j);
-      const int pid = __shfl_xor_sync(FULL, id, j);
-      const bool pbetter = pk > key || (pk == key && pid < id);
-      // in a descending block the lower lane of a pair keeps the better one
-      const bool keep_better = ((lane & j) == 0) == ((lane & kk) == 0);
-      const bool take = keep_better == pbetter;
-      key = take ? pk : key;
-      id = take ? pid : id;
+      const uint64_t p = __shfl_xor_sync(FULL, me, j);
+      // in a descending block the lower lane of a pair keeps the better one:
+      // take the partner's iff (p > me) == (bit j of lane == bit kk of lane)
+      const bool take = (p > me) ^ ((lane & j) != 0) ^ ((lane & kk) != 0);
+      me = take ? p : me;
     }
   }
+  return me;
 }
+
+// fkey of -inf: every selectable (finite or +inf) key is above it; lanes past
+// the queue end hold 0.
+constexpr uint32_t POP_KNEG = 0x007fffffu;
 
 static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__restrict__ logp, int32_t S, int64_t Q,
                                                                const int64_t *__restrict__ offsets,
@@ -457,16 +529,28 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
   const int n = (int)(offsets[q + 1] - offsets[q]);
   int bs = bs_q[q];
   bs = (bs >= 1 && bs <= S) ? bs : 0;
+  if (n <= 0 || !bs) {  // nothing selectable (warp-uniform)
+    sel[q * 32 + lane] = -1;
+    return;
+  }
+  // all 8 loads first and unconditional, so they are in flight together (a
+  // short queue's lanes past the end re-read its last member, masked below)
+  const float *row = logp + (int64_t)(bs - 1) * N + b0;
+  float v[8];
+  if (n >= 256) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = __ldg(row + 32 * s + lane);
+  } else {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = __ldg(row + min(32 * s + lane, n - 1));
+  }
   uint32_t k[8];
-  const float *row = logp + (int64_t)(bs ? bs - 1 : 0) * N + b0;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    const int r = 32 * s + lane;
-    k[s] = 0u;
-    if (r < n && bs) {
-      const float v = row[r];
-      k[s] = (v == -INFINITY || v != v) ? 0u : fkey(v + 0.0f);  // -0 + 0 = +0: -0 ties +0
-    }
+    // NaN -> -inf (never selected), -0 + 0 = +0 (-0 ties +0)
+    const uint32_t u = __float_as_uint(fmaxf(v[s] + 0.0f, -INFINITY));
+    const uint32_t key = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);  // fkey
+    k[s] = (n >= 256 || 32 * s + lane < n) ? key : 0u;
   }
   // lane head (first maximal slot) and the best other key
   uint32_t kh = k[0], k2 = 0u;
@@ -478,11 +562,12 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
     sh = gt ? s : sh;
     kh = gt ? k[s] : kh;
   }
-  if (__reduce_min_sync(FULL, kh) > __reduce_max_sync(FULL, k2)) {
-    uint32_t key = kh;
-    int id = 32 * sh + lane;
-    pop_bitonic32(key, id, lane);
-    sel[q * 32 + lane] = lane < bs ? id : -1;
+  // worst selectable head (all-ones if none) and best non-head
+  const uint32_t hsel = __reduce_min_sync(FULL, kh > POP_KNEG ? kh : 0xffffffffu);
+  const uint32_t mx2 = __reduce_max_sync(FULL, k2);
+  if (mx2 < hsel && (mx2 <= POP_KNEG || __popc(__ballot_sync(FULL, kh > POP_KNEG)) >= bs)) {
+    const uint64_t me = pop_bitonic32(((uint64_t)kh << 32) | (uint32_t)~(32 * sh + lane), lane);
+    sel[q * 32 + lane] = (lane < bs && (uint32_t)(me >> 32) > POP_KNEG) ? (int)~(uint32_t)me : -1;
     return;
   }
   int id[8];
@@ -504,7 +589,7 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
   int hid = id[0], pos = 0, mine = -1;
   for (int round = 0; round < bs; ++round) {
     const uint32_t mx = __reduce_max_sync(FULL, hk);
-    if (mx == 0u) break;  // no selectable member left (warp-uniform)
+    if (mx <= POP_KNEG) break;  // no selectable member left (warp-uniform)
     const int win = (int)__reduce_min_sync(FULL, hk == mx ? (uint32_t)hid : 0x7fffffffu);
     if (lane == round) mine = win;
     if (hid == win) {  // pop the head (member indices are distinct)

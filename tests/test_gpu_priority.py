@@ -250,23 +250,27 @@ def test_piecewise_step_scores_vs_oracle(name):
 
 
 def _fast_path_queues(off, v, bs):
-    """Queues on PopBatch's fast path (priority_kernel.cuh): min over lanes of
-    the lane-best key > max over lanes of every other key (order-preserving
-    keys, -inf / NaN / bs out of range -> not selectable).  Host restatement of
-    the kernel's warp-uniform test, used only to show both paths ran."""
+    """Queues on PopBatch's fast path (priority_kernel.cuh): every lane's best
+    other key below every selectable lane head, and either no selectable
+    non-head or at least bs selectable heads (order-preserving keys, -inf /
+    NaN not selectable).  Host restatement of the kernel's warp-uniform test,
+    used only to show both paths ran."""
     fast = np.zeros(len(bs), bool)
     for qi in range(len(bs)):
         b = int(bs[qi])
         n = int(off[qi + 1] - off[qi])
-        if not 1 <= b <= S or n < 32:
+        if not 1 <= b <= S or n <= 0:
             continue
-        x = np.full(256, -np.inf)
+        x = np.full(256, np.nan)  # lanes past the end: below every key
         x[:min(n, 256)] = v[off[qi]:off[qi] + min(n, 256), b - 1]
-        x[~np.isfinite(x) & ~(x > 0)] = -np.inf  # -inf / NaN: not selectable
-        lanes = x.reshape(8, 32)  # slot s, lane l: member 32 s + l
+        x = np.where(np.isnan(x) & (np.arange(256) < n), -np.inf, x)
+        lanes = np.where(np.isnan(x), -np.inf, x).reshape(8, 32)  # slot s, lane l: member 32 s + l
         head = lanes.max(axis=0)
         other = np.sort(lanes, axis=0)[-2]
-        fast[qi] = np.isfinite(head).all() and head.min() > other.max()
+        selh = head[head > -np.inf]
+        hsel = selh.min() if selh.size else np.inf
+        mx2 = other.max()
+        fast[qi] = mx2 < hsel and (mx2 == -np.inf or selh.size >= b)
     return fast
 
 
@@ -279,7 +283,7 @@ def test_pop_batch_fast_and_general_paths_bitexact():
     rng = np.random.default_rng(gen.SEED_BASE + 930)
     Q = 400
     lengths = rng.integers(32, 257, Q)
-    lengths[:6] = (32, 256, 256, 31, 5, 256)
+    lengths[:8] = (32, 256, 256, 31, 5, 256, 256, 256)
     off = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
     N = int(off[-1])
     v = np.empty((N, S), np.float32)
@@ -292,8 +296,12 @@ def test_pop_batch_fast_and_general_paths_bitexact():
     v[off[1]:off[2], :] = np.float32(-1.0)                   # 256 equal keys: each head ties its lane's next
     v[off[2]:off[2] + 32, :] = np.float32(-0.5)              # 32 equal heads, everything else lower
     v[off[2] + 32:off[3], :] = np.float32(-0.75)
+    v[off[6]:off[8], :] = -np.inf                             # only a few selectable members:
+    v[off[6] + 100:off[6] + 111, :] = np.float32(-2.0)        # 11 in distinct lanes (fast), and
+    v[off[7] + 100:off[7] + 111, :] = np.float32(-2.0)
+    v[off[7] + 132, :] = np.float32(-3.0)                     # one more behind a head (general)
     bs = rng.integers(1, S + 1, Q).astype(np.int32)
-    bs[:6] = (32, 32, 32, 32, 3, 17)
+    bs[:8] = (32, 32, 32, 32, 3, 17, 32, 32)
     q = orj.Queues.from_numpy(off, np.zeros(N), np.zeros(N), np.zeros(Q))
     fam = gen.gpt_family(gen.SEED_BASE + 915)
     store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
@@ -306,7 +314,7 @@ def test_pop_batch_fast_and_general_paths_bitexact():
         assert got == want, qi
         assert (sel[qi, len(got):] == -1).all()
     fast = _fast_path_queues(off, v, bs)
-    assert fast[2] and not fast[1] and not fast[3] and not fast[4]
+    assert fast[2] and fast[3] and fast[6] and not fast[1] and not fast[7]
     assert 0.3 < fast.mean() < 1.0, fast.mean()
     import _parity as par
     par.record("pop_batch_paths", label="unimodal+ties", queues=Q, fast_path=int(fast.sum()))
