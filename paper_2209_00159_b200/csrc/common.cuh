@@ -150,6 +150,15 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   return v;
 }
 
+// Non-volatile form for read-only phases: free to be scheduled among other
+// loads; the caller makes the address depend on a value produced after the
+// barrier that ends the writes (e.g. an opaque_u32 base taken after it).
+__device__ __forceinline__ float lds_f32_nv(uint32_t addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
 // ---- 32-bit shared-space arrays -------------------------------------------
 // A generic pointer into dynamic shared memory makes the compiler rebuild the
 // CTA's shared window base (S2UR CgaCtaId, ULEA, ...) at every access of a hot

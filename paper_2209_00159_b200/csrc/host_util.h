@@ -41,5 +41,33 @@ cudaError_t ensure_max_dyn_smem(K kernel, int bytes, std::atomic<uint64_t> &done
   return e;
 }
 
+// Resident blocks per SM x SM count (one wave) of a kernel at a block size and
+// dynamic shared memory, cached per device for the last smem size asked (the
+// occupancy query costs microseconds: not on every launch).  Races only
+// repeat the query.
+struct WaveCache {
+  std::atomic<int64_t> key[64];   // smem bytes + 1 (0: empty)
+  std::atomic<int64_t> wave[64];
+};
+template <class K>
+cudaError_t one_wave(K kernel, int threads, size_t smem, WaveCache &c, int64_t *out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && c.key[dev].load(std::memory_order_acquire) == (int64_t)smem + 1) {
+    *out = c.wave[dev].load(std::memory_order_relaxed);
+    return cudaSuccess;
+  }
+  int sms = 148, occ = 1;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem)) != cudaSuccess) return e;
+  *out = (int64_t)sms * (occ < 1 ? 1 : occ);
+  if (dev < 64) {
+    c.wave[dev].store(*out, std::memory_order_relaxed);
+    c.key[dev].store((int64_t)smem + 1, std::memory_order_release);
+  }
+  return cudaSuccess;
+}
+
 }  // namespace host
 }  // namespace orloj

@@ -239,13 +239,9 @@ cudaError_t prio_launch(unsigned grid, size_t smem, cudaStream_t s, const double
   if (e != cudaSuccess) return e;
   // one wave of resident blocks (grid-stride over queues): the per-size tables
   // are staged once per block
-  int dev = 0, sms = 148, occ = 1;
-  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 256,
-                                                         smem)) != cudaSuccess)
-    return e;
-  const int64_t cap = (int64_t)sms * (occ < 1 ? 1 : occ);
+  static WaveCache wc;
+  int64_t cap = 148;
+  if ((e = one_wave(priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 256, smem, wc, &cap)) != cudaSuccess) return e;
   grid = (unsigned)((int64_t)grid < cap ? grid : cap);
   priority_scores_kernel<SMEM_TABLE, STEPS, TIER><<<grid, 256, smem, s>>>(
       log_table, log_expected, S, B, b, prof, steps, cf, q->num_queues, q->queue_offsets, q->deadline_ticks,

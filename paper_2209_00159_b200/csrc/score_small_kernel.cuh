@@ -74,16 +74,28 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   for (int e = 0; e < BPL; ++e) bok[e] = lane + 32 * e < B;
   const uint32_t a_lane = smem_base(s_store) + 4u * lane;
   const SArr<float> dst{opaque_u32(smem_addr(lgs) + 4u * (1 + lane))};
+  if (K == 32 && B == 32 * BPL) {  // full queue, full bins (C2, C4): unrolled, unpredicated
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t src = a_lane + (uint32_t)__shfl_sync(FULL, idB, k);
+#pragma unroll
+      for (int e = 0; e < BPL; ++e) {
+        acc[e] += lds_f32_nv(src + 128u * e);
+        dst.st(k * ROW + 32 * e, acc[e]);
+      }
+    }
+  } else {
 #pragma unroll 8
   for (int k = 0; k < K; ++k) {
     const uint32_t src = a_lane + (uint32_t)__shfl_sync(FULL, idB, k);
 #pragma unroll
     for (int e = 0; e < BPL; ++e) {
       if (bok[e]) {
-        acc[e] += lds_f32(src + 128u * e);
+        acc[e] += lds_f32_nv(src + 128u * e);  // read-only store: free to issue ahead
         dst.st(k * ROW + 32 * e, acc[e]);
       }
     }
+  }
   }
   __syncwarp();
 
@@ -98,7 +110,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   for (int k = 1; k <= 32; ++k) {
     const int4 c = s_prof[k - 1];
     const int bi = lookup_bin(sig, c.x, c.y, (uint32_t)c.z, (uint32_t)c.w);
-    const float x = ex2_approx(lds_f32(row0 + 4u * (uint32_t)((k - 1) * ROW + bi)));
+    const float x = ex2_approx(lds_f32_nv(row0 + 4u * (uint32_t)((k - 1) * ROW + bi)));
     const float v = lane < k ? x : 0.f;  // members r <= k
     E = bfly_push(pend, v, k - 1, lane);
   }
