@@ -663,10 +663,31 @@ def run_c1_latency(dev):
                       "called through ctypes + stream synchronise), host clock"}
 
 
+MODEL_VARIANT_INSTR = os.path.join(ROOT, "profiles", "model_variants_instr.json")
+
+
+def model_variant_specs(cfg, prof):
+    """(name, duration table [kmax][B+1], interpolate, steps) of the C2 variants."""
+    B = cfg.fam.B
+    m = np.arange(B + 1, dtype=np.int64)
+    logm = np.round(B * (2.0 ** (4.0 * m / B) - 1.0) / 15.0).astype(np.int64)
+    tables = {"eq3": prof.a[:, None] + prof.w[:, None] * m[None, :],
+              "log_grid": prof.a[:, None] + prof.w[:, None] * logm[None, :]}
+    steps = ([-cfg.fam.p99_ticks() // 4, 0, cfg.fam.p99_ticks() // 2], [0.25, 1.0, 1.5])
+    return [("eq3/edge/1 step", tables["eq3"], False, None), ("eq3/uniform/1 step", tables["eq3"], True, None),
+            ("eq3/edge/3 steps", tables["eq3"], False, steps),
+            ("log_grid/uniform/3 steps", tables["log_grid"], True, steps)]
+
+
 def run_model_variants(dev, max_over_ranks, world):
     """Scoring-model variants on the C2 shape: 1,024
     SkipNet-like queues x 64, kmax 32, B 64 (orloj_score_model_batches, one
-    launch per pick, 100 picks per CUDA graph)."""
+    launch per pick, 100 picks per CUDA graph).  Issue roofline per variant:
+    the warp instructions of one launch (ncu, profiles/model_variants_instr.json,
+    re-captured with scripts/gpu_model.sh whenever the model kernels change)
+    over this run's time per pick, against the 148 x 4-scheduler issue peak."""
+    import json
+
     import torch
 
     import gen
@@ -677,18 +698,15 @@ def run_model_variants(dev, max_over_ranks, world):
     store = wl.score_store(cfg, dev)
     qs = wl.device_queues(cfg.queues, dev, with_arrival=False)
     prof = wl.profile(cfg.profile)
-    B, Q = cfg.fam.B, cfg.queues.Q
-    m = np.arange(B + 1, dtype=np.int64)
-    logm = np.round(B * (2.0 ** (4.0 * m / B) - 1.0) / 15.0).astype(np.int64)
-    tables = {"eq3": prof.a[:, None] + prof.w[:, None] * m[None, :],
-              "log_grid": prof.a[:, None] + prof.w[:, None] * logm[None, :]}
-    steps = ([-cfg.fam.p99_ticks() // 4, 0, cfg.fam.p99_ticks() // 2], [0.25, 1.0, 1.5])
+    Q = cfg.queues.Q
+    instr = {}
+    if os.path.exists(MODEL_VARIANT_INSTR):
+        with open(MODEL_VARIANT_INSTR) as f:
+            instr = json.load(f).get("instructions_per_launch", {})
     res = {}
     stream = torch.cuda.Stream(dev)
-    for name, tab, interp, st in (("eq3/edge/1 step", "eq3", False, None), ("eq3/uniform/1 step", "eq3", True, None),
-                                  ("eq3/edge/3 steps", "eq3", False, steps),
-                                  ("log_grid/uniform/3 steps", "log_grid", True, steps)):
-        model = orj.ScoreModel(tables[tab], interpolate=interp, steps=st, device=dev)
+    for name, tab, interp, st in model_variant_specs(cfg, prof):
+        model = orj.ScoreModel(tab, interpolate=interp, steps=st, device=dev)
         buf = {"E": torch.empty((Q, model.kmax), dtype=torch.float32, device=dev),
                "best_k": torch.empty(Q, dtype=torch.int32, device=dev),
                "best_E": torch.empty(Q, dtype=torch.float32, device=dev)}
@@ -710,6 +728,12 @@ def run_model_variants(dev, max_over_ranks, world):
         torch.cuda.synchronize()
         ms = max_over_ranks(e0.elapsed_time(e1)) / 1000
         res[name] = {"us_per_pick": 1e3 * ms, "decisions_per_s": world * Q / (ms / 1e3)}
+        if name in instr:
+            ach = instr[name] / (ms / 1e3) / 1e12
+            peak = 148 * 4 * 1965e6 / 1e12
+            res[name]["roofline"] = {"bound": "issue", "achieved": ach, "peak": peak, "unit": "T warp-instructions/s",
+                                     "frac": ach / peak, "instructions_per_launch": instr[name],
+                                     "instructions_source": "profiles/model_variants_instr.json (ncu)"}
     del store, qs
     return res
 

@@ -481,10 +481,23 @@ typedef struct {
   int32_t num_steps;
   const int64_t *step_offset_ticks;
   const double *step_cost;
+  const void *plan; /* device ORLOJ_SCORE_MODEL_PLAN_BYTES from orloj_score_model_prepare for this
+                       duration table (reused across calls), or NULL: analysed on every call */
 } orloj_score_model;
 orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_queues *queues,
                                        const orloj_score_model *model, float *expected_finish, int32_t *best_k,
                                        float *best_expected, void *stream);
+
+/* Analyse a duration table once (async on `stream`): for each size k, whether
+ * its row is an arithmetic grid dur[m] = dur[0] + w m (Eq. 3; w >= 1,
+ * dur[0] >= 0, dur[0] + w B < 2^30), and if so the constants of the main
+ * scorer's exact integer lookup (floor((x - dur[0]) / w) by a division magic)
+ * that orloj_score_model_batches then uses instead of a binary search over the
+ * row -- the same bin, so the same results.  plan: device buffer of
+ * ORLOJ_SCORE_MODEL_PLAN_BYTES (caller-owned; valid while the table is
+ * unchanged).  model->plan is ignored here. */
+#define ORLOJ_SCORE_MODEL_PLAN_BYTES 512
+orloj_status orloj_score_model_prepare(const orloj_score_model *model, int32_t num_bins, void *plan, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Validation (synchronous, O(N), not hot; may allocate a few bytes of scratch).

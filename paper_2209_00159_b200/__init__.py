@@ -335,6 +335,12 @@ class ScoreModel:
             self.cost = np.ascontiguousarray(steps[1], dtype=np.float64)
             if self.off.shape != self.cost.shape or self.off.ndim != 1:
                 raise OrlojError(1, "steps: offsets and costs must be 1-D of equal length")
+        # the table's row analysis, once (orloj_score_model_prepare), reused by every score call
+        self.plan = torch.empty(_abi.SCORE_MODEL_PLAN_BYTES, dtype=torch.uint8, device=self.dur.device)
+        self._c = _abi.ScoreModelC(self.kmax, self.dur.data_ptr(), int(self.interpolate), 0, None, None, None)
+        _abi.check(_abi.lib().orloj_score_model_prepare(ctypes.byref(self._c), self.num_bins, self.plan.data_ptr(),
+                                                        _stream_ptr(None)))
+        torch.cuda.current_stream(self.dur.device).synchronize()  # the plan is read on any stream later
 
     @classmethod
     def eq3(cls, profile: "LatencyProfile", num_bins: int, **kw) -> "ScoreModel":
@@ -345,7 +351,7 @@ class ScoreModel:
     def c(self):
         self._c = _abi.ScoreModelC(self.kmax, self.dur.data_ptr(), int(self.interpolate), len(self.off),
                                    self.off.ctypes.data if len(self.off) else None,
-                                   self.cost.ctypes.data if len(self.cost) else None)
+                                   self.cost.ctypes.data if len(self.cost) else None, self.plan.data_ptr())
         return ctypes.byref(self._c)
 
     def score(self, store: HistogramStore, queues: Queues, stream=None, out: Optional[dict] = None) -> dict:

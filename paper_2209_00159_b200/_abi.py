@@ -91,9 +91,13 @@ class CostSteps(ctypes.Structure):
     _fields_ = [("num_steps", ctypes.c_int32), ("offset_ticks", ctypes.c_void_p), ("cost", ctypes.c_void_p)]
 
 
+SCORE_MODEL_PLAN_BYTES = 512  # ORLOJ_SCORE_MODEL_PLAN_BYTES
+
+
 class ScoreModelC(ctypes.Structure):
     _fields_ = [("kmax", ctypes.c_int32), ("duration_ticks", ctypes.c_void_p), ("interpolate", ctypes.c_int32),
-                ("num_steps", ctypes.c_int32), ("step_offset_ticks", ctypes.c_void_p), ("step_cost", ctypes.c_void_p)]
+                ("num_steps", ctypes.c_int32), ("step_offset_ticks", ctypes.c_void_p), ("step_cost", ctypes.c_void_p),
+                ("plan", ctypes.c_void_p)]
 
 
 class ReplayEpochC(ctypes.Structure):
@@ -135,6 +139,7 @@ SIGNATURES = {
                                               ctypes.c_int64, _P, ctypes.c_size_t, _P, _P, _P]),
     "orloj_score_model_batches": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(QueuesC),
                                                  ctypes.POINTER(ScoreModelC), _P, _P, _P, _P]),
+    "orloj_score_model_prepare": (ctypes.c_int, [ctypes.POINTER(ScoreModelC), ctypes.c_int32, _P, _P]),
     "orloj_priority_table": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,
                                             _P, ctypes.c_double, _P, _P, _P]),
     "orloj_priority_scores": (ctypes.c_int, [ctypes.POINTER(Store), ctypes.POINTER(LatencyProfile), ctypes.c_int32,

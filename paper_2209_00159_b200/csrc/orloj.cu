@@ -511,15 +511,52 @@ orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_que
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned grid = (unsigned)((p.Q + MODEL_WARPS - 1) / MODEL_WARPS);
   cudaError_t e;
+  // row analysis (arithmetic grids -> exact division): the caller's plan, or a
+  // stream-ordered scratch analysed now
+  ModelRow *rows = nullptr;
+  if (model->plan) {
+    p.rows = static_cast<const ModelRow *>(model->plan);
+  } else {
+    if (cudaMallocAsync((void **)&rows, 32 * sizeof(ModelRow), s) != cudaSuccess)
+      return fail(ORLOJ_ERR_OOM, "score model: cannot allocate the row scratch");
+    model_prep_kernel<<<1, 256, 0, s>>>(p.dur, p.kmax, p.B, rows);
+    p.rows = rows;
+  }
+  const bool one = p.nsteps == 1 && p.off[0] == 0 && p.dc[0] == 1.f;
   if (model->interpolate) {
     e = cudaFuncSetAttribute(model_score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) model_score_kernel<true><<<grid, MODEL_WARPS * 32, smem, s>>>(p);
   } else {
-    e = cudaFuncSetAttribute(model_score_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) model_score_kernel<false><<<grid, MODEL_WARPS * 32, smem, s>>>(p);
+    // upper-edge model: the score_small layout (rows first, butterfly sums), B <= 32 BPL
+    const int bpl = p.B <= 32 ? 1 : p.B <= 64 ? 2 : 4;
+    const size_t sm = bpl == 1 ? ModelEdgeShape<1>::bytes(p.kmax, p.B, p.D, p.smem_store)
+                      : bpl == 2 ? ModelEdgeShape<2>::bytes(p.kmax, p.B, p.D, p.smem_store)
+                                 : ModelEdgeShape<4>::bytes(p.kmax, p.B, p.D, p.smem_store);
+    auto go = [&](auto kern) {
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (r == cudaSuccess) kern<<<grid, MODEL_WARPS * 32, sm, s>>>(p);
+      return r;
+    };
+    if (bpl == 1) e = one ? go(model_edge_kernel<1, true>) : go(model_edge_kernel<1, false>);
+    else if (bpl == 2) e = one ? go(model_edge_kernel<2, true>) : go(model_edge_kernel<2, false>);
+    else e = one ? go(model_edge_kernel<4, true>) : go(model_edge_kernel<4, false>);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
+  if (rows) cudaFreeAsync(rows, s);
   if (e != cudaSuccess) return cuda_fail(e, "score_model launch");
+  return ok();
+}
+
+orloj_status orloj_score_model_prepare(const orloj_score_model *model, int32_t num_bins, void *plan, void *stream) {
+  static_assert(32 * sizeof(ModelRow) <= ORLOJ_SCORE_MODEL_PLAN_BYTES, "plan size");
+  if (!model || model->kmax < 1 || model->kmax > 32 || !model->duration_ticks || !plan || num_bins < 1 ||
+      num_bins > MODEL_MAX_BINS)
+    return fail(ORLOJ_ERR_INVALID_ARGUMENT, "score_model_prepare: need a model (1 <= kmax <= 32), 1 <= B <= %d, plan",
+                MODEL_MAX_BINS);
+  model_prep_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(model->duration_ticks, model->kmax, num_bins,
+                                                          static_cast<ModelRow *>(plan));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "score_model_prepare launch");
   return ok();
 }
 
