@@ -41,6 +41,12 @@ WORKLOAD = ("C3: 65,536 queues x 256 requests x 256-bin per-request histograms (
             "mean 774.66 / P99 1101.99 ms), kmax = 256, 16.8 M permuted 1 KB rows (17.2 GB store)")
 
 
+def nvtx(name):
+    """NVTX range around a bench leg (nsys attribution; a no-op without a tool)."""
+    import torch
+    return torch.cuda.nvtx.range(name)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -471,11 +477,13 @@ def main():
 
     # ---------------- other workload shapes (C2 SkipNet-like, C4 static CNN) ----------------
     if not args.no_extra:
-        result["workloads"] = run_other_workloads(args, dev, max_over_ranks, world)
+        with nvtx("workloads"):
+            result["workloads"] = run_other_workloads(args, dev, max_over_ranks, world)
 
     # ---------------- replay sweep (C5) ----------------
     if not args.no_replay:
-        result["replay"] = run_replay(args, rank, world, dev, barrier, max_over_ranks)
+        with nvtx("replay"):
+            result["replay"] = run_replay(args, rank, world, dev, barrier, max_over_ranks)
 
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -541,10 +549,14 @@ def run_other_workloads(args, dev, max_over_ranks, world):
             out[name]["agreement_with_planner"] = float((bk.cpu().numpy() == planner_k).mean())
         del store, qs
     torch.cuda.empty_cache()
-    out["C2-HBM"] = run_c2_hbm(dev, max_over_ranks, world, c2_best_k)
-    out["C1_latency"] = run_c1_latency(dev)
-    out["P1"] = run_priority(dev, max_over_ranks, world)
-    out["C2_model_variants"] = run_model_variants(dev, max_over_ranks, world)
+    with nvtx("C2-HBM"):
+        out["C2-HBM"] = run_c2_hbm(dev, max_over_ranks, world, c2_best_k)
+    with nvtx("C1_latency"):
+        out["C1_latency"] = run_c1_latency(dev)
+    with nvtx("P1"):
+        out["P1"] = run_priority(dev, max_over_ranks, world)
+    with nvtx("C2_model_variants"):
+        out["C2_model_variants"] = run_model_variants(dev, max_over_ranks, world)
     return out
 
 
@@ -1115,9 +1127,12 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
                            "instructions_source": "profiles/replay_sweep_launches.csv (ncu smsp__inst_executed.sum)",
                            "peak_source": "148 SMs x 4 warp schedulers x 1 instruction/cycle at sm_max_mhz"}
     if not args.no_policies:
-        out["policies"] = run_policies(args, rank, world, dev)
-        out["b_sweep"] = run_b_sweep(args, rank, world, dev)
-        out["feedback"] = run_feedback(args, rank, world, dev)
+        with nvtx("policies"):
+            out["policies"] = run_policies(args, rank, world, dev)
+        with nvtx("b_sweep"):
+            out["b_sweep"] = run_b_sweep(args, rank, world, dev)
+        with nvtx("feedback"):
+            out["feedback"] = run_feedback(args, rank, world, dev)
     if world == 1 and not args.no_shard_proxy:
         # strong-scaling proxy on one GPU: time EVERY rank's shard of an N-GPU run
         # (median of 3 sweeps each; everything but the ~10 us all-reduce) and take

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys, ncu) injects
 #include <cstddef>
 #include <cstdint>
 
@@ -40,6 +42,17 @@ cudaError_t ensure_max_dyn_smem(K kernel, int bytes, std::atomic<uint64_t> &done
   if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
   return e;
 }
+
+// One NVTX range per C-ABI call (push at entry, pop at return), so nsys / ncu
+// timelines attribute the multi-stream replay and the e2e copy pipelines to
+// the library calls that enqueued them.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define ORLOJ_NVTX(name) ::orloj::host::NvtxRange orloj_nvtx_range_(name)
 
 // Resident blocks per SM x SM count (one wave) of a kernel at a block size and
 // dynamic shared memory, cached per device for the last smem size asked (the

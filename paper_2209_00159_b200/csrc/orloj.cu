@@ -350,6 +350,7 @@ const char *orloj_last_error(void) { return g_last_error.c_str(); }
 int32_t orloj_abi_version(void) { return ORLOJ_ABI_VERSION; }
 
 orloj_status orloj_store_build(const uint32_t *counts, int32_t D, int32_t B, float *out, void *stream) {
+  ORLOJ_NVTX("orloj_store_build");
   if (!counts || !out || D < 1 || B < 4 || B % 4)
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store_build: need counts, out, D >= 1, B a positive multiple of 4");
   if (B > ORLOJ_MAX_BINS) return fail(ORLOJ_ERR_CAPACITY, "store_build: B=%d > %d", B, ORLOJ_MAX_BINS);
@@ -368,6 +369,7 @@ orloj_status orloj_store_build(const uint32_t *counts, int32_t D, int32_t B, flo
 
 orloj_status orloj_score_batches(const orloj_store *store, const orloj_latency_profile *profile,
                                  const orloj_queues *queues, float *E, float *P, float *EL, void *stream) {
+  ORLOJ_NVTX("orloj_score_batches");
   ScoreParams p;
   orloj_status st = prepare_score(store, profile, queues, &p);
   if (st) return st;
@@ -383,6 +385,7 @@ orloj_status orloj_score_batches(const orloj_store *store, const orloj_latency_p
 
 orloj_status orloj_pick_batch(const orloj_store *store, const orloj_latency_profile *profile,
                               const orloj_queues *queues, int32_t *best_k, float *best_E, void *stream) {
+  ORLOJ_NVTX("orloj_pick_batch");
   ScoreParams p;
   orloj_status st = prepare_score(store, profile, queues, &p);
   if (st) return st;
@@ -407,6 +410,7 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
                                    const int64_t *off_h, const int64_t *dl_h, const int32_t *dist_h,
                                    const int64_t *now_h, int32_t *bk_h, float *bE_h, void *ws, size_t ws_bytes,
                                    void *stream) {
+  ORLOJ_NVTX("orloj_pick_batch_host");
   if (Q < 0 || !off_h || (Q > 0 && (!now_h || !bk_h || !bE_h)))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pick_batch_host: bad host arrays");
   const int64_t N = off_h[Q] - off_h[0];
@@ -463,6 +467,7 @@ orloj_status orloj_pick_batch_host(const orloj_store *store, const orloj_latency
 orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_queues *queues,
                                        const orloj_score_model *model, float *E, int32_t *best_k, float *best_E,
                                        void *stream) {
+  ORLOJ_NVTX("orloj_score_model_batches");
   orloj_status st;
   if ((st = check_store(store, MODEL_MAX_BINS))) return st;
   if ((st = check_queues(queues))) return st;
@@ -548,6 +553,7 @@ orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_que
 }
 
 orloj_status orloj_score_model_prepare(const orloj_score_model *model, int32_t num_bins, void *plan, void *stream) {
+  ORLOJ_NVTX("orloj_score_model_prepare");
   static_assert(32 * sizeof(ModelRow) <= ORLOJ_SCORE_MODEL_PLAN_BYTES, "plan size");
   if (!model || model->kmax < 1 || model->kmax > 32 || !model->duration_ticks || !plan || num_bins < 1 ||
       num_bins > MODEL_MAX_BINS)
@@ -563,6 +569,7 @@ orloj_status orloj_score_model_prepare(const orloj_score_model *model, int32_t n
 orloj_status orloj_priority_table(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
                                   const float *weights, double b, double *log_table, double *log_expected,
                                   void *stream) {
+  ORLOJ_NVTX("orloj_priority_table");
   orloj_status st;
   if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
   ProfileDev prof;
@@ -585,6 +592,7 @@ orloj_status orloj_priority_table(const orloj_store *store, const orloj_latency_
 orloj_status orloj_priority_scores(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
                                    double b, const double *log_table, const double *log_expected,
                                    const orloj_queues *queues, float *out, void *stream) {
+  ORLOJ_NVTX("orloj_priority_scores");
   return priority_scores_impl(store, profile, S, b, log_table, log_expected, queues, nullptr, out, stream);
 }
 
@@ -592,12 +600,14 @@ orloj_status orloj_priority_scores_steps(const orloj_store *store, const orloj_l
                                          double b, const double *log_table, const double *log_expected,
                                          const orloj_queues *queues, const orloj_cost_steps *steps, float *out,
                                          void *stream) {
+  ORLOJ_NVTX("orloj_priority_scores_steps");
   if (!steps) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "priority_scores_steps: steps is NULL");
   return priority_scores_impl(store, profile, S, b, log_table, log_expected, queues, steps, out, stream);
 }
 
 orloj_status orloj_pop_batch(const orloj_queues *queues, const float *logp, int32_t S, const int32_t *bs,
                              int32_t *sel, void *stream) {
+  ORLOJ_NVTX("orloj_pop_batch");
   orloj_status st;
   if ((st = check_queues(queues))) return st;
   if (S < 1) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pop_batch: num_sizes < 1");
@@ -613,6 +623,7 @@ orloj_status orloj_pop_batch(const orloj_queues *queues, const float *logp, int3
 
 orloj_status orloj_histogram_accumulate(const int32_t *dist_id, const int64_t *solo_ticks, int64_t n,
                                         int64_t bin_ticks, uint32_t *counts, int32_t D, int32_t B, void *stream) {
+  ORLOJ_NVTX("orloj_histogram_accumulate");
   if (n < 0 || D < 1 || B < 1 || bin_ticks <= 0 || !counts || (n > 0 && (!dist_id || !solo_ticks)))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "histogram_accumulate: bad sizes or pointers");
   if ((int64_t)D * B > (1ll << 30)) return fail(ORLOJ_ERR_CAPACITY, "histogram_accumulate: D*B too large");
@@ -631,6 +642,7 @@ orloj_status orloj_histogram_accumulate(const int32_t *dist_id, const int64_t *s
 orloj_status orloj_profile_outcomes(const int32_t *dist_id, const int16_t *true_bin, const uint8_t *outcome,
                                     const uint8_t *sample_mask, int64_t n, uint32_t *counts, int32_t D, int32_t B,
                                     void *stream) {
+  ORLOJ_NVTX("orloj_profile_outcomes");
   if (n < 0 || D < 1 || B < 1 || !counts || (n > 0 && (!dist_id || !true_bin || !outcome)))
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "profile_outcomes: bad sizes or pointers");
   if ((int64_t)D * B > (1ll << 30)) return fail(ORLOJ_ERR_CAPACITY, "profile_outcomes: D*B too large");
@@ -648,6 +660,7 @@ orloj_status orloj_profile_outcomes(const int32_t *dist_id, const int16_t *true_
 
 orloj_status orloj_store_refresh(const uint32_t *counts, int32_t D, int32_t B, uint32_t min_samples, float *out,
                                  void *stream) {
+  ORLOJ_NVTX("orloj_store_refresh");
   if (!counts || !out || D < 1 || B < 4 || B % 4)
     return fail(ORLOJ_ERR_INVALID_ARGUMENT, "store_refresh: need counts, out, D >= 1, B a positive multiple of 4");
   if (B > ORLOJ_MAX_BINS) return fail(ORLOJ_ERR_CAPACITY, "store_refresh: B=%d > %d", B, ORLOJ_MAX_BINS);
@@ -661,6 +674,7 @@ orloj_status orloj_store_refresh(const uint32_t *counts, int32_t D, int32_t B, u
 }
 
 orloj_status orloj_validate_store(const orloj_store *store, void *stream) {
+  ORLOJ_NVTX("orloj_validate_store");
   orloj_status st;
   if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -674,6 +688,7 @@ orloj_status orloj_validate_store(const orloj_store *store, void *stream) {
 }
 
 orloj_status orloj_validate_queues(const orloj_store *store, const orloj_queues *q, void *stream) {
+  ORLOJ_NVTX("orloj_validate_queues");
   orloj_status st;
   if ((st = check_store(store, ORLOJ_MAX_BINS))) return st;
   if ((st = check_queues(q))) return st;
@@ -691,6 +706,7 @@ orloj_status orloj_validate_queues(const orloj_store *store, const orloj_queues 
 }
 
 orloj_status orloj_validate_trace(const orloj_store *store, const orloj_trace *tr, void *stream) {
+  ORLOJ_NVTX("orloj_validate_trace");
   orloj_status st;
   if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
   if (!tr || tr->num_scenarios < 0 || tr->num_buckets < 1)

@@ -131,6 +131,7 @@ size_t orloj_replay_seg_workspace(int64_t num_scenarios, int64_t num_arrivals, i
 
 orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_profile *profile,
                                 const orloj_trace *tr, orloj_counters *per_bucket, int32_t *log, void *stream) {
+  ORLOJ_NVTX("orloj_replay_trace");
   const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
   return orloj_replay_trace_ex(store, profile, tr, &def, per_bucket, log, stream);
 }
@@ -138,6 +139,7 @@ orloj_status orloj_replay_trace(const orloj_store *store, const orloj_latency_pr
 orloj_status orloj_replay_trace_ex(const orloj_store *store, const orloj_latency_profile *profile,
                                    const orloj_trace *tr, const orloj_replay_policy *policy,
                                    orloj_counters *per_bucket, int32_t *log, void *stream) {
+  ORLOJ_NVTX("orloj_replay_trace_ex");
   return replay_impl(store, profile, tr, policy, 1, 0, nullptr, 0, per_bucket, log, stream);
 }
 
@@ -145,6 +147,7 @@ orloj_status orloj_replay_trace_seg(const orloj_store *store, const orloj_latenc
                                     const orloj_trace *tr, const orloj_replay_policy *policy, int32_t segments,
                                     int64_t num_arrivals, void *workspace, size_t workspace_bytes, orloj_counters *per_bucket,
                                     int32_t *log, void *stream) {
+  ORLOJ_NVTX("orloj_replay_trace_seg");
   const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
   return replay_impl(store, profile, tr, policy ? policy : &def, segments, num_arrivals, workspace, workspace_bytes, per_bucket,
                      log, stream);
@@ -154,6 +157,7 @@ orloj_status orloj_replay_trace_epoch(const orloj_store *store, const orloj_late
                                       const orloj_trace *tr, const orloj_replay_policy *policy,
                                       const orloj_replay_epoch *epoch, orloj_counters *per_bucket, int32_t *log,
                                       void *stream) {
+  ORLOJ_NVTX("orloj_replay_trace_epoch");
   const orloj_replay_policy def{ORLOJ_OBJ_EXPECTED_FINISH, nullptr, nullptr, nullptr, nullptr, 0.0};
   if (!epoch) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "replay_trace_epoch: epoch descriptor is NULL");
   return replay_impl(store, profile, tr, policy ? policy : &def, 1, 0, nullptr, 0, per_bucket, log, stream, epoch);
@@ -171,6 +175,7 @@ orloj_status orloj_replay_feedback(const orloj_store *store, const orloj_latency
                                    const orloj_feedback *fb, void *workspace, size_t workspace_bytes,
                                    orloj_counters *per_epoch_bucket, uint32_t *window_counts_out,
                                    int32_t *decision_logs, void *stream) {
+  ORLOJ_NVTX("orloj_replay_feedback");
   orloj_status st;
   if ((st = check_store(store, ORLOJ_REPLAY_MAX_BINS))) return st;
   if (!fb || fb->num_epochs < 1 || fb->window_epochs < 1 || fb->min_samples < 1)

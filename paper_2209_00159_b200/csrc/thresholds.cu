@@ -193,6 +193,7 @@ extern "C" {
 
 orloj_status orloj_expected_latency_thresholds(const uint32_t *counts, int32_t D, int32_t B,
                                                const orloj_latency_profile *profile, int64_t *thr) {
+  ORLOJ_NVTX("orloj_expected_latency_thresholds");
   std::vector<uint64_t> tot;
   orloj_status st;
   if ((st = check_counts(counts, D, B, &tot))) return st;
@@ -211,6 +212,7 @@ orloj_status orloj_expected_latency_thresholds(const uint32_t *counts, int32_t D
 
 orloj_status orloj_alg1_size_thresholds(const uint32_t *counts, int32_t D, int32_t B, const double *weights,
                                         const orloj_latency_profile *profile, int64_t *thr) {
+  ORLOJ_NVTX("orloj_alg1_size_thresholds");
   std::vector<uint64_t> tot;
   orloj_status st;
   if ((st = check_counts(counts, D, B, &tot))) return st;
