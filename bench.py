@@ -817,6 +817,23 @@ def build_replay(args, rank, world, dev):
                         device=dev) for name in gen.C5_FAMILIES]
 
 
+def family_segments(spec, name: str):
+    """Per-family segment spec: "auto", an int, or "fam=G,...[,default]" (e.g.
+    "rdi=16,auto"): the family's own entry, else the default (auto)."""
+    spec = str(spec)
+    if "=" not in spec:
+        return spec
+    default = "auto"
+    for part in spec.split(","):
+        if "=" in part:
+            k, v = part.split("=", 1)
+            if k.strip() == name:
+                return v.strip()
+        elif part.strip():
+            default = part.strip()
+    return default
+
+
 def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
     """Segments per scenario for the segmented replay.  "auto": 8 per scenario
     while a family has >= 1,024 scenarios on this rank, 16 from 512, else 24
@@ -869,8 +886,8 @@ def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True, segments=
     streams = [torch.cuda.Stream(dev) for _ in fams]
     main = torch.cuda.current_stream()
     tables = torch.zeros((len(fams), nb, 7), dtype=torch.int64, device=dev)
-    segs = [replay_segments(segments, f.trace.num_scenarios, f.trace.num_arrivals // max(f.trace.num_scenarios, 1))
-            for f in fams]
+    segs = [replay_segments(family_segments(segments, f.tf.fam.name), f.trace.num_scenarios,
+                            f.trace.num_arrivals // max(f.trace.num_scenarios, 1)) for f in fams]
     wss = [torch.empty(max(orj.replay_seg_workspace_bytes(f.trace, g), 1), dtype=torch.uint8, device=dev)
            for f, g in zip(fams, segs)]   # allocated once, outside the timed region
 
