@@ -50,6 +50,30 @@ def main():
     tab.pop(q, lp, torch.tensor([3], dtype=torch.int32, device="cuda"))
     for interp in (False, True):
         orj.ScoreModel.eq3(pr, st.num_bins, interpolate=interp, steps=([0, 300], [1.0, 1.5])).score(st, q)
+    # round-2 paths: short-queue full-queue build (C4 shape), priority TIER 0 / 1 with the
+    # vector member map and both PopBatch paths, the model edge kernel (grid rows, a
+    # non-grid row, several steps)
+    c4 = gen.config4(Q=40)
+    st4 = orj.HistogramStore.from_counts(c4.fam.counts, c4.fam.bin_ticks)
+    orj.pick_batch(st4, wl.profile(c4.profile), wl.device_queues(c4.queues))
+    cp = gen.config_priority(Q=12, n=256)
+    cp.queues.offsets[6:] -= 3  # a short queue and unaligned chunks next to full ones
+    stp = orj.HistogramStore.from_counts(cp.fam.counts, cp.fam.bin_ticks)
+    qp = wl.device_queues(cp.queues)
+    for b in (1.0 / cp.fam.mean_ticks(), 50.0 / cp.fam.mean_ticks()):
+        tp = orj.PriorityTable(stp, wl.profile(cp.profile), 32, b)
+        lpp = tp.scores(qp)
+        tp.pop(qp, lpp, torch.full((cp.queues.Q,), 32, dtype=torch.int32, device="cuda"))
+        tp.pop(qp, torch.zeros_like(lpp), torch.full((cp.queues.Q,), 5, dtype=torch.int32, device="cuda"))
+    c2 = gen.config2(Q=16)
+    st2 = orj.HistogramStore.from_counts(c2.fam.counts, c2.fam.bin_ticks)
+    q2 = wl.device_queues(c2.queues)
+    m = np.arange(c2.fam.B + 1, dtype=np.int64)
+    eq3 = c2.profile.a[:, None] + c2.profile.w[:, None] * m[None, :]
+    logm = eq3.copy()
+    logm[3] = c2.profile.a[3] + c2.profile.w[3] * np.round(c2.fam.B * (2.0 ** (4.0 * m / c2.fam.B) - 1.0) / 15.0).astype(np.int64)
+    for tab_, st_ in ((eq3, None), (eq3, ([0, 300], [1.0, 1.5])), (logm, None), (logm, ([0, 300], [1.0, 1.5]))):
+        orj.ScoreModel(tab_, steps=st_).score(st2, q2)
     prof = orj.Profiler(st.num_dists, st.num_bins, st.bin_ticks)
     prof.add(torch.tensor([0, 1, 2], dtype=torch.int32, device="cuda"),
              torch.tensor([5, 1500, 99999], dtype=torch.int64, device="cuda"))
