@@ -233,7 +233,7 @@ template <bool SMEM_TABLE, bool STEPS, int TIER>
 cudaError_t prio_launch(unsigned grid, size_t smem, cudaStream_t s, const double *log_table,
                         const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
                         const StepsDev &steps, const PrioCoef &cf, const orloj_queues *q, float *out,
-                        const float2 *gtab) {
+                        const void *gtab) {
   static std::atomic<uint64_t> configured{0};  // per instantiation and device
   cudaError_t e = ensure_max_dyn_smem(priority_scores_kernel<SMEM_TABLE, STEPS, TIER>, 96 << 10, configured);
   if (e != cudaSuccess) return e;
@@ -253,7 +253,7 @@ template <bool SMEM_TABLE, bool STEPS>
 cudaError_t prio_launch_tier(int tier, unsigned grid, size_t smem, cudaStream_t s, const double *log_table,
                              const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
                              const StepsDev &steps, const PrioCoef &cf, const orloj_queues *q, float *out,
-                             const float2 *gtab) {
+                             const void *gtab) {
   return tier == 0 ? prio_launch<SMEM_TABLE, STEPS, 0>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
                                                         cf, q, out, gtab)
                    : prio_launch<SMEM_TABLE, STEPS, 1>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
@@ -295,8 +295,6 @@ orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_
   // Grid-stride over queues: ~resident blocks, so the per-size constants are
   // staged once per block, not once per 8 queues.
   const int B = store->num_bins;
-  const bool smem_table = PrioSmem::table_bytes(S, B) <= (88u << 10);
-  const size_t smem = PrioSmem::bytes(S, B, smem_table);
   const int64_t want = (queues->num_queues + 7) / 8;
   const unsigned grid = (unsigned)(want < (1 << 30) ? want : (1 << 30));  // capped at one wave in prio_launch
   // Tier (priority_kernel.cuh): TIER 0 (strict-count lookup, fitted g) when
@@ -310,14 +308,18 @@ orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_
   for (int k = 0; k < S && t0; ++k) t0 = (int64_t)prof.a[k] + (int64_t)prof.w[k] * B + 1 <= cap0;
   const int tier = t0 ? 0 : 1;
   cf.half_b = (float)(b / 2.0);
+  cf.half_b_log2e = (float)(b / 2.0 * 1.4426950408889634);
   cf.gb = (float)(-std::expm1(-b));
   cf.cap = t0 ? (int32_t)cap0 : 0x3fffffff;
+  // the re-based table in shared memory when it fits the budget, else in global memory
+  const bool smem_table = PrioSmem::table_bytes(S, B, tier) <= (88u << 10);
+  const size_t smem = PrioSmem::bytes(S, B, smem_table, tier);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  float2 *gtab = nullptr;
+  void *gtab = nullptr;
   if (!smem_table) {
     const int64_t ne = (int64_t)S * (B + 2);
-    if (cudaMallocAsync((void **)&gtab, (size_t)ne * sizeof(float2), s) != cudaSuccess)
+    if (cudaMallocAsync(&gtab, (size_t)ne * PrioSmem::entry_bytes(tier), s) != cudaSuccess)
       return fail(ORLOJ_ERR_OOM, "priority_scores: cannot allocate the re-based table");
     if (tier == 0)
       priority_rebase_kernel<0><<<(unsigned)((ne + 255) / 256), 256, 0, s>>>(log_table, log_expected, S, B, b, prof,

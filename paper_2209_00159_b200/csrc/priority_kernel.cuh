@@ -17,6 +17,8 @@
 //           - log E[L].
 // C changes only at the milestones sigma = l_i: p(t) = alpha e^{bt} + beta.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace orloj {
@@ -113,10 +115,14 @@ static __global__ void priority_table_kernel(const float *__restrict__ log2F, in
 // b (sigma - cap) in a warp-uniform slow path.
 // Output [S][N] (size-major: each store of a warp is one contiguous 128-B line,
 // and PopBatch reads one size row coalesced).
+// Table entries: TIER 0 float4 {C', H', D2 = (C' - H') log2 e, 0} (the log-add-exp's
+// exponent in one FFMA), TIER 1 float2 {C', H'}.
+template <int TIER> using PrioEntry = typename std::conditional<TIER == 0, float4, float2>::type;
 struct PrioSmem {
-  static __host__ __device__ size_t table_bytes(int S, int B) { return (size_t)S * (B + 2) * 8; }
-  static __host__ __device__ size_t bytes(int S, int B, bool smem_table) {
-    return (size_t)S * (16 + 8) + (smem_table ? table_bytes(S, B) : 0);
+  static __host__ __device__ size_t entry_bytes(int tier) { return tier == 0 ? 16 : 8; }
+  static __host__ __device__ size_t table_bytes(int S, int B, int tier) { return (size_t)S * (B + 2) * entry_bytes(tier); }
+  static __host__ __device__ size_t bytes(int S, int B, bool smem_table, int tier) {
+    return (size_t)S * (16 + 8) + (smem_table ? table_bytes(S, B, tier) : 0);
   }
 };
 
@@ -174,8 +180,10 @@ __device__ __forceinline__ float prio_elem_global(const double *__restrict__ tab
 }
 
 constexpr int PRIO_CHUNK = 8;  // members per lane per pass
-#ifndef PRIO_MIN_BLOCKS
-#define PRIO_MIN_BLOCKS  // experiments: -DPRIO_MIN_BLOCKS=,5 caps registers for 5 resident blocks per SM
+#ifdef PRIO_MIN_BLOCKS  // experiments: -DPRIO_MIN_BLOCKS=5 caps registers for 5 resident blocks per SM
+#define PRIO_BOUNDS __launch_bounds__(256, PRIO_MIN_BLOCKS)
+#else
+#define PRIO_BOUNDS __launch_bounds__(256)
 #endif
 constexpr int PRIO_MAX_STEPS = 8;
 
@@ -191,6 +199,7 @@ struct StepsDev {
 // Per-call constants of the g tiers (host-computed in fp64, rounded once).
 struct PrioCoef {
   float half_b;  // b / 2
+  float half_b_log2e;  // b / 2 log2 e
   float gb;      // 1 - e^{-b}
   float c[6];    // P(u) = c0 + c1 u + ... + c5 u^5 (TIER 0, host-fitted)
   int32_t cap;   // slack cap (ticks) of the tier's lookup
@@ -217,21 +226,26 @@ __device__ __forceinline__ int4 prio_lk(const ProfileDev &prof, int k, int B) {
 
 // Re-based table entry (k, e) of the tier (layout above; stride B+2).
 template <int TIER>
-__device__ __forceinline__ float2 prio_entry(const double *__restrict__ table, const double *__restrict__ logEL,
-                                             const ProfileDev &prof, int B, double b, int k, int e) {
+__device__ __forceinline__ PrioEntry<TIER> prio_entry(const double *__restrict__ table,
+                                                      const double *__restrict__ logEL, const ProfileDev &prof, int B,
+                                                      double b, int k, int e) {
   const double lEL = logEL[k];
   const double *tab = table + (size_t)k * 2 * (B + 1);
   const double a = prof.a[k], w = prof.w[k];
-  if (TIER == 0) {
-    if (e == 0) return make_float2(-INFINITY, -INFINITY);
+  if constexpr (TIER == 0) {
+    // D2 = (C' - H') log2 e from the fp64 values, rounded once (NaN when both are -inf:
+    // prio_combine's clamp then gives -inf, the value of p = 0)
+    if (e == 0) return make_float4(-INFINITY, -INFINITY, NAN, 0.f);
     const double C = tab[e - 1];
-    return make_float2(C == -INFINITY ? -INFINITY : (float)(C - b * (a + w * (e - 1)) - b - lEL),
-                       e <= B ? (float)(tab[B + 1 + e] - lEL) : -INFINITY);
+    const double Cr = C == -INFINITY ? -INFINITY : C - b * (a + w * (e - 1)) - b - lEL;
+    const double Hr = e <= B ? tab[B + 1 + e] - lEL : -INFINITY;
+    return make_float4((float)Cr, (float)Hr, (float)((Cr - Hr) * 1.4426950408889634), 0.f);
+  } else {
+    if (e > B) return make_float2(-INFINITY, -INFINITY);  // unused pad
+    const double C = tab[e];
+    return make_float2(C == -INFINITY ? -INFINITY : (float)(C - b * (a + w * e) - lEL),
+                       e < B ? (float)(tab[B + 1 + e + 1] - lEL) : -INFINITY);
   }
-  if (e > B) return make_float2(-INFINITY, -INFINITY);  // unused pad
-  const double C = tab[e];
-  return make_float2(C == -INFINITY ? -INFINITY : (float)(C - b * (a + w * e) - lEL),
-                     e < B ? (float)(tab[B + 1 + e + 1] - lEL) : -INFINITY);
 }
 
 // Table row of one size: shared (a 32-bit shared-space address taken after the
@@ -239,16 +253,32 @@ __device__ __forceinline__ float2 prio_entry(const double *__restrict__ table, c
 // barrier) or global (tables above the shared-memory budget).
 struct PrioTabS {
   uint32_t base;
-  __device__ __forceinline__ float2 ld(int j) const {
-    float2 v;
-    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(base + 8u * (uint32_t)j));
+  template <class E>
+  __device__ __forceinline__ E ld(int j) const {
+    E v;
+    if constexpr (sizeof(E) == 16)
+      asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+          : "r"(base + 16u * (uint32_t)j));
+    else
+      asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(base + 8u * (uint32_t)j));
     return v;
   }
 };
 struct PrioTabG {
-  const float2 *p;
-  __device__ __forceinline__ float2 ld(int j) const { return __ldg(p + j); }
+  const unsigned char *p;  // row base (entries of the tier's type)
+  template <class E>
+  __device__ __forceinline__ E ld(int j) const { return __ldg(reinterpret_cast<const E *>(p) + j); }
 };
+
+// The log-add-exp of TIER 0 with its exponent d2 = (lp - Hn) log2 e given:
+// log(e^lp + e^Hn g) = (d2 >= 0 ? lp : Hn) + log(1 + 2^-|d2| g  or  2^-|d2| + g)
+// (prio_combine with d2 from one FFMA of the table's D2; the same clamp).
+__device__ __forceinline__ float prio_combine_d2(float lp, float Hn, float d2, float g) {
+  const float e = ex2_approx(fmaxf(-fabsf(d2), -150.f));
+  const bool hi = !(d2 < 0.f);  // NaN (lp = Hn = -inf) -> hi: y = 1, lp = -inf
+  const float y = hi ? fmaf(e, g, 1.f) : e + g;
+  return fmaf(0.6931471805599453f, lg2_approx(y), hi ? lp : Hn);
+}
 
 // log p of one (member, size): s2 = prio_s2(sigma), tk the size's re-based
 // table row, bxe = b (sigma - cap) above the cap, else 0.
@@ -259,16 +289,17 @@ __device__ __forceinline__ float prio_elem(const Tab &tk, const int4 &lk, int32_
   int32_t xc = x2 < lk.y ? x2 : lk.y;
   xc = xc > 0 ? xc : 0;
   const int j = (int)(__umulhi((uint32_t)xc, (uint32_t)lk.z) >> (uint32_t)lk.w);
-  const float2 T = tk.ld(j);
-  if (TIER == 0) {
+  const PrioEntry<TIER> T = tk.template ld<PrioEntry<TIER>>(j);
+  if constexpr (TIER == 0) {
     const float u = (float)(x2 + nw * j);  // 2 (x - 1), x = sigma - l1_j
     const float lp = fmaf(-cf.half_b, u, T.x) - bxe;
+    const float d2 = fmaf(-cf.half_b_log2e, u, T.z) - bxe * 1.4426950408889634f;  // (lp - Hn) log2 e
     float c = fmaf(cf.c[5], u, cf.c[4]);
     c = fmaf(c, u, cf.c[3]);
     c = fmaf(c, u, cf.c[2]);
     c = fmaf(c, u, cf.c[1]);
     c = fmaf(c, u, cf.c[0]);
-    return prio_combine(lp, T.y, fmaf(u, c, cf.gb));
+    return prio_combine_d2(lp, T.y, d2, fmaf(u, c, cf.gb));
   } else {
     const int32_t x = (x2 >> 1) + nw * j;  // sigma - l2_i
     const float Hn = x > 0 ? T.y : -INFINITY;
@@ -286,15 +317,15 @@ __device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const in
                                            double b, float bf, const PrioCoef &cf, const StepsDev &steps);
 
 template <bool SMEM_TABLE, bool STEPS, int TIER>
-__global__ void __launch_bounds__(256 PRIO_MIN_BLOCKS) priority_scores_kernel(
+__global__ void PRIO_BOUNDS priority_scores_kernel(
     const double *__restrict__ table, const double *__restrict__ logEL, int32_t S, int32_t B, double b,
     const __grid_constant__ ProfileDev prof, const __grid_constant__ StepsDev steps, const PrioCoef cf, int64_t Q,
     const int64_t *__restrict__ offsets, const int64_t *__restrict__ deadline, const int64_t *__restrict__ now,
-    float *__restrict__ out, const float2 *__restrict__ gtab) {
+    float *__restrict__ out, const void *__restrict__ gtab) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int4 *s_lk = reinterpret_cast<int4 *>(smem_raw);       // [S]
   int2 *s_wk = reinterpret_cast<int2 *>(s_lk + S);      // [S] {nw, unused}
-  float2 *s_T = reinterpret_cast<float2 *>(s_wk + S);   // [S][B+2] (SMEM_TABLE)
+  PrioEntry<TIER> *s_T = reinterpret_cast<PrioEntry<TIER> *>(s_wk + S);  // [S][B+2] (SMEM_TABLE)
   for (int k = threadIdx.x; k < S; k += blockDim.x) {
     s_lk[k] = prio_lk<TIER>(prof, k, B);
     s_wk[k] = make_int2(TIER == 0 ? -2 * prof.w[k] : -prof.w[k], 0);
@@ -364,10 +395,12 @@ __global__ void __launch_bounds__(256 PRIO_MIN_BLOCKS) priority_scores_kernel(
       const unsigned mode = (over ? 1u : 0u) | (__all_sync(0xffffffffu, nv == PRIO_CHUNK) ? 2u : 0u) | (vec ? 4u : 0u);
       float *out0 = out + c0 + (vec ? 4 * lane : lane);
       if (SMEM_TABLE)
-        prio_chunk<TIER, STEPS>(PrioTabS{smem_base(s_T)}, 8 * (B + 2), s_lk, s_wk, S, out0, N, nv, mode, sg, s2, bxe,
-                                b, bf, cf, steps);
+        prio_chunk<TIER, STEPS>(PrioTabS{smem_base(s_T)}, (int32_t)sizeof(PrioEntry<TIER>) * (B + 2), s_lk, s_wk, S,
+                                out0, N, nv, mode, sg, s2, bxe, b, bf, cf, steps);
       else
-        prio_chunk<TIER, STEPS>(PrioTabG{gtab}, B + 2, s_lk, s_wk, S, out0, N, nv, mode, sg, s2, bxe, b, bf, cf, steps);
+        prio_chunk<TIER, STEPS>(PrioTabG{static_cast<const unsigned char *>(gtab)},
+                                (int32_t)sizeof(PrioEntry<TIER>) * (B + 2), s_lk, s_wk, S, out0, N, nv, mode, sg, s2,
+                                bxe, b, bf, cf, steps);
     }
   }
 }
@@ -401,7 +434,7 @@ __device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const in
   Tab tk = t0;
   auto step = [&]() {
     if constexpr (sizeof(Tab) == sizeof(uint32_t)) tk.base += (uint32_t)rowb;
-    else tk.p += rowb;
+    else tk.p += rowb;  // bytes
   };
   if (STEPS) {
     for (int k = 0; k < S; ++k, step()) {
@@ -454,11 +487,11 @@ __device__ __forceinline__ void prio_chunk(const Tab &t0, int32_t rowb, const in
 template <int TIER>
 __global__ void priority_rebase_kernel(const double *__restrict__ table, const double *__restrict__ logEL, int32_t S,
                                        int32_t B, double b, const __grid_constant__ ProfileDev prof,
-                                       float2 *__restrict__ gtab) {
+                                       void *__restrict__ gtab) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)S * (B + 2)) return;
   const int k = (int)(e / (B + 2));
-  gtab[e] = prio_entry<TIER>(table, logEL, prof, B, b, k, (int)(e - (int64_t)k * (B + 2)));
+  static_cast<PrioEntry<TIER> *>(gtab)[e] = prio_entry<TIER>(table, logEL, prof, B, b, k, (int)(e - (int64_t)k * (B + 2)));
 }
 
 // Compare-exchange for a descending sort of (key, -index) pairs: after it,
