@@ -25,6 +25,19 @@
 #pragma once
 #include "common.cuh"
 
+// Unroll of the k-group loop inside a 32-k chunk (8 groups of G = 4).  Fully
+// unrolled (8) keeps every ring-slot index and butterfly level compile-time,
+// but the C3 pick kernel is then 6,136 SASS instructions with a 3,275-
+// instruction hot loop, and ncu showed no_instruction (instruction-fetch)
+// stalls; unrolled by 2 it is ~2,000 instructions and the C3 pick went from
+// 2.94 to 2.51 ms on one box (1 / 2 / 4 / 8: 2.71 / 2.51 / 2.61 / 2.94 ms).
+#ifndef ORLOJ_SCORE_KG_UNROLL
+#define ORLOJ_SCORE_KG_UNROLL 2
+#endif
+namespace orloj {
+constexpr int SCORE_KG_UNROLL = ORLOJ_SCORE_KG_UNROLL;
+}
+
 namespace orloj {
 
 struct ScoreParams {
@@ -155,7 +168,7 @@ score_kernel(const __grid_constant__ ScoreParams p) {
     float pend[5];
     float pendL[5];
     float Ek = 0.f, Sk = 0.f;
-#pragma unroll
+#pragma unroll SCORE_KG_UNROLL
     for (int kg = 0; kg < 32; kg += G) {
       // one group of G consecutive k = k0 .. k0+G-1 (rows j0 .. j0+G-1, one barrier)
       const int k0 = 32 * c + kg + 1;
