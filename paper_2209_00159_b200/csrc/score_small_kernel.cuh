@@ -45,6 +45,18 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   int4 *s_prof = reinterpret_cast<int4 *>(s_dyn + (((size_t)D * B + 3) & ~(size_t)3));
   float *lgs = reinterpret_cast<float *>(s_prof + 32) + wid * 32 * ROW;  // row k-1 = LG_k
 
+  // the queue's offsets / now are requested before the block stages the store,
+  // so their latency overlaps the staging and the barrier
+  const int64_t q = (int64_t)blockIdx.x * SMALL_WARPS + wid;
+  const bool live = q < p.Q;
+  int64_t o0 = 0, o1 = 0, now = 0;
+  if (live) {
+    o0 = p.offsets[q];
+    o1 = p.offsets[q + 1];
+    now = p.now[q];
+  }
+  const int64_t base0 = p.offsets[0];  // offsets may start at any base (chunked calls)
+
   for (int e = threadIdx.x * 4; e < D * B; e += blockDim.x * 4)
     *reinterpret_cast<float4 *>(s_store + e) = __ldg(reinterpret_cast<const float4 *>(p.log2F + e));
   if (threadIdx.x < 32) {  // sizes beyond kmax: constants that look up bin 0 (never counted)
@@ -55,14 +67,20 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   lgs[lane * ROW] = -INFINITY;
   __syncthreads();
 
-  const int64_t q = (int64_t)blockIdx.x * SMALL_WARPS + wid;
-  if (q >= p.Q) return;
-  const int64_t off = p.offsets[q] - p.offsets[0];  // offsets may start at any base (chunked calls)
-  const int64_t n = p.offsets[q + 1] - p.offsets[q];
+  if (!live) return;
+  const int64_t off = o0 - base0;
+  const int64_t n = o1 - o0;
   const int K = (int)(n < kmax ? n : kmax);
-  const int64_t now = p.now[q];
-  const int32_t sig = lane < K ? sigma2(p.deadline[off + lane] - now) : 0;
-  const int idB = lane < K ? p.dist[off + lane] * B * 4 : 0;  // byte offset of member lane's row
+  // both member loads unconditional (a lane past the end re-reads the last member, masked below)
+  int64_t dl = 0;
+  int32_t dd = 0;
+  if (n > 0) {
+    const int64_t j = off + (lane < n ? lane : n - 1);
+    dl = p.deadline[j];
+    dd = p.dist[j];
+  }
+  const int32_t sig = lane < K ? sigma2(dl - now) : 0;
+  const int idB = lane < K ? dd * B * 4 : 0;  // byte offset of member lane's row
 
   // a2: LG_k for k = 1..K, lanes over bins (bin lane + 32 e + 1); 32-bit
   // shared-space addresses (common.cuh SArr), kept in registers
