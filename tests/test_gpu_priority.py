@@ -318,3 +318,33 @@ def test_pop_batch_fast_and_general_paths_bitexact():
     assert 0.3 < fast.mean() < 1.0, fast.mean()
     import _parity as par
     par.record("pop_batch_paths", label="unimodal+ties", queues=Q, fast_path=int(fast.sum()))
+
+
+def test_scores_vector_map_equals_scalar_map():
+    """P1-shaped queues (256 members, 4-aligned starts) take the 16-byte vector
+    member map; the same queues shifted by one member (a 1-member queue in
+    front) take the strided map.  Same element arithmetic: bit-identical
+    scores.  A sample is checked against the oracle as well."""
+    cfg = gen.config_priority(Q=24, n=256)
+    q = cfg.queues
+    b = 1.0 / cfg.fam.mean_ticks()
+    store = orj.HistogramStore.from_counts(cfg.fam.counts, cfg.fam.bin_ticks)
+    p = orj.LatencyProfile(cfg.profile.a, cfg.profile.w)
+    tab = orj.PriorityTable(store, p, S, b)
+    lp_vec = tab.scores(wl.device_queues(q))
+    off2 = np.concatenate([[0], np.asarray(q.offsets) + 1]).astype(np.int64)
+    dl2 = np.concatenate([[int(q.now[0]) + 1000], np.asarray(q.deadline)]).astype(np.int64)
+    dist2 = np.concatenate([[0], np.asarray(q.dist)]).astype(np.int32)
+    now2 = np.concatenate([[int(q.now[0])], np.asarray(q.now)]).astype(np.int64)
+    lp_sc = tab.scores(orj.Queues.from_numpy(off2, dl2, dist2, now2))
+    torch.cuda.synchronize()
+    assert torch.equal(lp_vec, lp_sc[:, 1:])
+    got = lp_vec.cpu().numpy().T.astype(np.float64)
+    sub = np.arange(0, 3)
+    o = np.asarray(q.offsets)
+    ref = pr.scores(cfg.fam.counts, cfg.profile.a, cfg.profile.w, S, b, o[:4], q.deadline[:o[3]], q.now[:3],
+                    store_fp32=True)
+    g = got[:o[3]]
+    ninf = ref == -np.inf
+    assert (np.isneginf(g) == ninf).all()
+    assert (np.abs(g[~ninf] - ref[~ninf]) <= _tol(ref[~ninf])).all()

@@ -86,6 +86,36 @@ def test_eq3_edge_unit_step_matches_main_scorer():
     torch.cuda.synchronize()
     k = torch.arange(1, KMAX + 1, device="cuda")
     assert ((main - var).abs() <= 1e-5 * k).all()
+    # the edge kernel on an arithmetic-grid table is the short-queue scorer's
+    # arithmetic step for step (same adds, lookup constants, ex2, butterfly)
+    assert torch.equal(main, var)
+
+
+def test_model_without_plan_equals_planned():
+    """orloj_score_model_batches with plan = NULL (row analysis on every call)
+    gives the planned call's results bit for bit, for a grid table and for a
+    table with a non-grid row (binary search), one and three steps."""
+    import ctypes
+    from paper_2209_00159_b200 import _abi
+    fam, prof, q = _case(gen.SEED_BASE + 953)
+    store = orj.HistogramStore.from_counts(fam.counts, fam.bin_ticks)
+    qs = wl.device_queues(q)
+    t = _tables(fam, prof)
+    mixed = t["eq3"].copy()
+    mixed[5] = t["log"][5]
+    for dur in (t["eq3"], mixed):
+        for steps in (None, ([-200, 0, 900], [0.25, 1.0, 1.5])):
+            model = orj.ScoreModel(dur, steps=steps)
+            planned = model.score(store, qs)
+            c = model.c()
+            c._obj.plan = None
+            E = torch.empty_like(planned["E"])
+            bk = torch.empty_like(planned["best_k"])
+            bE = torch.empty_like(planned["best_E"])
+            _abi.check(_abi.lib().orloj_score_model_batches(store.c(), qs.c(), c, E.data_ptr(), bk.data_ptr(),
+                                                            bE.data_ptr(), torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+            assert torch.equal(E, planned["E"]) and torch.equal(bk, planned["best_k"])
 
 
 def test_invalid_models():
