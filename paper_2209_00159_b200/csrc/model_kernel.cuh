@@ -17,8 +17,8 @@
 // a row is searched by the main scorer's exact integer division (umulhi by a
 // magic constant, common.cuh lookup_bin) instead of the 8-step binary search
 // -- the same m, so the same results.  The upper-edge model runs in
-// model_edge_kernel (the main short-queue scorer's layout); model_score_kernel
-// serves the within-bin-uniform (interpolated) model.  Not the C3 hot kernel:
+// model_edge_kernel (the main short-queue scorer's layout), the within-bin-
+// uniform (interpolated) one in model_interp_kernel.  Not the C3 hot kernel:
 // a variant for C2-sized workloads.
 #pragma once
 #include "common.cuh"
@@ -58,9 +58,10 @@ struct ModelParams {
   float *best_E;     // [Q] or null
 };
 
+// shared memory of model_interp_kernel
 __host__ __device__ inline size_t model_smem_bytes(int kmax, int B, int D, bool smem_store) {
   return (size_t)kmax * (B + 1) * 8 + (size_t)32 * sizeof(ModelRow) + (smem_store ? (size_t)D * B * 4 : 0) +
-         (size_t)MODEL_WARPS * ((B + 4) * 4 + 32 * 4 + 32 * 33 * 4);
+         (size_t)MODEL_WARPS * (32 * 4 + 32 * 33 * 4);
 }
 
 // One block (orloj_score_model_prepare, or once per call without a plan): mark
@@ -97,27 +98,46 @@ static __global__ void model_prep_kernel(const int64_t *__restrict__ dur, int km
   }
 }
 
-template <bool INTERP>
-__global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __grid_constant__ ModelParams p) {
+// Largest m in 0..B with dk[m] <= x (0 if none): branch-free binary search with
+// a fixed trip count (rows non-decreasing in m).  Out of line: the edge kernel
+// unrolls its size loop, and only a row that is not an arithmetic grid calls it.
+__device__ __forceinline__ int model_search_inl(const int64_t *dk, int B, int64_t x) {
+  int lo = 0;
+#pragma unroll
+  for (int s2 = MODEL_MAX_BINS; s2 > 0; s2 >>= 1)
+    if (lo + s2 <= B && dk[lo + s2] <= x) lo += s2;
+  return lo;
+}
+__device__ __noinline__ int model_search(const int64_t *dk, int B, int64_t x) {
+  int lo = 0;
+#pragma unroll
+  for (int s2 = MODEL_MAX_BINS; s2 > 0; s2 >>= 1)
+    if (lo + s2 <= B && dk[lo + s2] <= x) lo += s2;
+  return lo;
+}
+
+// Within-bin-uniform (interpolated) model: P_r(k) = prod_{j<=k} F_j^lin(m + u)
+// is not a prefix sum of logs, so no LG rows: warp per queue, for k = 1..K
+// lanes r < k evaluate their own product over the members j <= k (O(K^3) per
+// queue, the model's own cost); per-k partial sums reduced once after the loop.
+__global__ void __launch_bounds__(MODEL_WARPS * 32) model_interp_kernel(const __grid_constant__ ModelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int B = p.B, kmax = p.kmax;
-  int64_t *s_dur = reinterpret_cast<int64_t *>(smem_raw);                     // [kmax][B+1]
+  int64_t *s_dur = reinterpret_cast<int64_t *>(smem_raw);                          // [kmax][B+1]
   ModelRow *s_row = reinterpret_cast<ModelRow *>(s_dur + (size_t)kmax * (B + 1));  // [32]
-  float *s_store = reinterpret_cast<float *>(s_row + 32);                      // [D][B] (smem_store)
+  float *s_store = reinterpret_cast<float *>(s_row + 32);                           // [D][B] (smem_store)
   float *s_warp = s_store + (p.smem_store ? (size_t)p.D * B : 0);
   for (int e = threadIdx.x; e < kmax * (B + 1); e += blockDim.x) s_dur[e] = p.dur[e];
-  // the interpolated model reads F itself: stage 2^{log2 F} (the same ex2_approx
-  // per entry as an in-loop conversion, once per block instead of per use)
+  // the model reads F itself: stage 2^{log2 F} (the same ex2_approx per entry as
+  // an in-loop conversion, once per block instead of per use)
   if (p.smem_store)
-    for (int e = threadIdx.x; e < p.D * B; e += blockDim.x)
-      s_store[e] = INTERP ? ex2_approx(p.log2F[e]) : p.log2F[e];
+    for (int e = threadIdx.x; e < p.D * B; e += blockDim.x) s_store[e] = ex2_approx(p.log2F[e]);
   if (threadIdx.x < 32) s_row[threadIdx.x] = p.rows[threadIdx.x];
   __syncthreads();
   const float *store = p.smem_store ? s_store : p.log2F;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  float *stg = s_warp + wid * ((B + 4) + 32 + 32 * 33) + 4;  // LG_k row, stg[-1] unused
-  int32_t *s_d = reinterpret_cast<int32_t *>(stg + B);  // member distributions [32]
-  float *part = reinterpret_cast<float *>(s_d + 32);      // [k-1][lane] partial sums, stride 33
+  int32_t *s_d = reinterpret_cast<int32_t *>(s_warp + wid * (32 + 32 * 33));  // member distributions [32]
+  float *part = reinterpret_cast<float *>(s_d + 32);                           // [k-1][lane] partials, stride 33
   const int64_t q = (int64_t)blockIdx.x * MODEL_WARPS + wid;
   if (q >= p.Q) return;
   const int64_t base0 = p.offsets[0];
@@ -126,69 +146,39 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __g
   const int K = n < kmax ? n : kmax;
   const int64_t t = p.now[q];
   const int64_t sig = lane < K ? p.deadline[b0 + lane] - t : 0;
-  const int dr = lane < K ? p.dist[b0 + lane] : 0;
-  s_d[lane] = dr;
+  s_d[lane] = lane < K ? p.dist[b0 + lane] : 0;
   __syncwarp();
-  float lg[MODEL_MAX_BINS / 32];
-#pragma unroll
-  for (int v = 0; v < MODEL_MAX_BINS / 32; ++v) lg[v] = 0.f;
   for (int k = 1; k <= K; ++k) {
     const int64_t *dk = s_dur + (size_t)(k - 1) * (B + 1);
     const ModelRow rk = s_row[k - 1];
-    if (!INTERP) {
-      const int d = s_d[k - 1];
-#pragma unroll
-      for (int v = 0; v < MODEL_MAX_BINS / 32; ++v) {
-        const int e = 32 * v + lane;
-        if (e < B) {
-          lg[v] += store[(size_t)d * B + e];
-          stg[e] = lg[v];
-        }
-      }
-      __syncwarp();
-    }
     float acc = 0.f;
     if (lane < k) {
-      for (int s = 0; s < p.nsteps; ++s) {
-        const int64_t x = sig + p.off[s];
+      for (int st = 0; st < p.nsteps; ++st) {
+        const int64_t x = sig + p.off[st];
+        // largest m in 0..B with dur[k][m] <= x (0 if none): exact division on a
+        // grid row (warp-uniform), else the fixed-trip binary search
+        const int lo = model_lin(rk) ? model_lookup(rk, sigma2(x)) : model_search_inl(dk, B, x);
         float P;
-        // largest m in 0..B with dur[k][m] <= x (0 if none)
-        int lo = 0;
-        if (model_lin(rk)) {  // warp-uniform: floor((x - a) / w) clamped to [0, B], exact (common.cuh lookup_bin)
-          lo = model_lookup(rk, sigma2(x));
-        } else {  // branch-free binary search with a fixed trip count (rows non-decreasing in m)
-#pragma unroll
-          for (int st = MODEL_MAX_BINS; st > 0; st >>= 1)
-            if (lo + st <= B && dk[lo + st] <= x) lo += st;
-        }
-        if (!INTERP) {
-          // i* = #{m in 1..B : dur[k][m] <= x}  (A1: mass at the upper edges)
-          P = lo == 0 ? 0.f : ex2_approx(stg[lo - 1]);
-        } else {
-          // largest m in 0..B with dur[k][m] <= x; position m + u inside the grid
-          if (x < dk[0]) {
-            P = 0.f;
-          } else {
-            if (lo == B) {
-              P = 1.f;
-            } else {
-              const float u = (float)((double)(x - dk[lo]) / (double)(dk[lo + 1] - dk[lo]));
-              P = 1.f;
-              for (int j = 0; j < k; ++j) {
-                const float *row = store + (size_t)s_d[j] * B;
-                const float f0 = lo == 0 ? 0.f : (p.smem_store ? row[lo - 1] : ex2_approx(row[lo - 1]));
-                const float f1 = p.smem_store ? row[lo] : ex2_approx(row[lo]);
-                P *= fmaf(u, f1 - f0, f0);
-              }
-            }
+        if (x < dk[0]) {
+          P = 0.f;
+        } else if (lo == B) {
+          P = 1.f;
+        } else {  // position m + u inside the grid
+          const float u = (float)((double)(x - dk[lo]) / (double)(dk[lo + 1] - dk[lo]));
+          P = 1.f;
+          for (int j = 0; j < k; ++j) {
+            const float *row = store + (size_t)s_d[j] * B;
+            const float f0 = lo == 0 ? 0.f : (p.smem_store ? row[lo - 1] : ex2_approx(row[lo - 1]));
+            const float f1 = p.smem_store ? row[lo] : ex2_approx(row[lo]);
+            P *= fmaf(u, f1 - f0, f0);
           }
         }
-        acc = fmaf(p.dc[s], P, acc);
+        acc = fmaf(p.dc[st], P, acc);
       }
     }
     part[(k - 1) * 33 + lane] = acc;  // reduced after the loop: no shuffle chain per k
-    __syncwarp();
   }
+  __syncwarp();
   // E_k in lane k-1: sum of the members' partials (lanes >= k contributed 0)
   float E = 0.f;
   if (lane < K)
@@ -205,16 +195,6 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_score_kernel(const __g
   }
 }
 
-// Largest m in 0..B with dk[m] <= x (0 if none): branch-free binary search with
-// a fixed trip count (rows non-decreasing in m).  Out of line: the edge kernel
-// unrolls its size loop, and only a row that is not an arithmetic grid calls it.
-__device__ __noinline__ int model_search(const int64_t *dk, int B, int64_t x) {
-  int lo = 0;
-#pragma unroll
-  for (int s2 = MODEL_MAX_BINS; s2 > 0; s2 >>= 1)
-    if (lo + s2 <= B && dk[lo + s2] <= x) lo += s2;
-  return lo;
-}
 
 // Upper-edge bin model (interpolate = 0), the score_small_kernel layout
 // (score_small_kernel.cuh): the warp builds LG_1..LG_K of its queue first

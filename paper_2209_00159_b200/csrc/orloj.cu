@@ -531,8 +531,8 @@ orloj_status orloj_score_model_batches(const orloj_store *store, const orloj_que
   }
   const bool one = p.nsteps == 1 && p.off[0] == 0 && p.dc[0] == 1.f;
   if (model->interpolate) {
-    e = cudaFuncSetAttribute(model_score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) model_score_kernel<true><<<grid, MODEL_WARPS * 32, smem, s>>>(p);
+    e = cudaFuncSetAttribute(model_interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) model_interp_kernel<<<grid, MODEL_WARPS * 32, smem, s>>>(p);
   } else {
     // upper-edge model: the score_small layout (rows first, butterfly sums), B <= 32 BPL
     const int bpl = p.B <= 32 ? 1 : p.B <= 64 ? 2 : 4;
