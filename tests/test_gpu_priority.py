@@ -348,3 +348,35 @@ def test_scores_vector_map_equals_scalar_map():
     ninf = ref == -np.inf
     assert (np.isneginf(g) == ninf).all()
     assert (np.abs(g[~ninf] - ref[~ninf]) <= _tol(ref[~ninf])).all()
+
+
+@pytest.mark.parametrize("b_scale", [1.0, 20.0])
+def test_scores_slack_beyond_the_cap(b_scale):
+    """Members whose slack exceeds the lookup's 2^30-tick cap (the warp-uniform
+    slow path adds b (sigma - cap) in fp32) and members far past their deadline,
+    in both tiers (b_scale 1: the fitted-polynomial tier, 20: the general one),
+    in aligned full queues (vector map) and ragged ones."""
+    fam = gen.gpt_family(gen.SEED_BASE + 960)
+    prof = gen.eq3_half(fam, S)
+    rng = np.random.default_rng(gen.SEED_BASE + 961)
+    lengths = np.array([256, 256, 37, 256, 5, 256], np.int64)
+    q = gen.snapshot_queues(gen.SEED_BASE + 962, lengths, fam.p99_ticks(), D=fam.D)
+    o = np.asarray(q.offsets)
+    dl = np.asarray(q.deadline).copy()
+    for qq in range(len(lengths)):
+        seg = slice(o[qq], o[qq + 1])
+        far = rng.random(o[qq + 1] - o[qq]) < 0.3
+        dl[seg][far] = int(q.now[qq]) + (1 << 30) + rng.integers(0, 1 << 33, far.sum())
+        past = rng.random(o[qq + 1] - o[qq]) < 0.1
+        dl[seg][past] = int(q.now[qq]) - rng.integers(1, 1 << 20, past.sum())
+    for qq in range(len(lengths)):  # keep each queue deadline-ordered
+        dl[o[qq]:o[qq + 1]] = np.sort(dl[o[qq]:o[qq + 1]])
+    q.deadline = dl
+    b = b_scale / fam.mean_ticks()
+    _, _, lp = _gpu_scores(fam, prof, q, b)
+    got = lp.cpu().numpy().T.astype(np.float64)
+    ref = pr.scores(fam.counts, prof.a, prof.w, S, b, q.offsets, q.deadline, q.now, store_fp32=True)
+    ninf = ref == -np.inf
+    assert (np.isneginf(got) == ninf).all()
+    err = np.abs(got[~ninf] - ref[~ninf])
+    assert (err <= _tol(ref[~ninf])).all(), float(err.max())
