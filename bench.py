@@ -70,8 +70,8 @@ def parse():
     ap.add_argument("--no-policies", action="store_true", help="skip the replay policy-variant sweep")
     ap.add_argument("--policy-seeds", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=32)
-    ap.add_argument("--e2e-streams", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=12)
+    ap.add_argument("--e2e-streams", type=int, default=2)
     ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 workload lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -44,7 +44,7 @@ def main():
     h_dist = torch.from_numpy(qn.dist).pin_memory()
     h_now = torch.from_numpy(qn.now).pin_memory()
     stream = torch.cuda.Stream()
-    for chunks, streams in ((16, 2), (32, 2), (32, 3), (64, 3), (64, 4), (128, 4)):
+    for chunks, streams in ((4, 2), (8, 2), (8, 3), (12, 2), (16, 2), (16, 3), (24, 2), (32, 3)):
         hp = orj.HostPicker(store, prof, qn.offsets, chunks=chunks, streams=streams)
         for _ in range(3):
             hp.pick(h_off, h_dl, h_dist, h_now, stream)
