@@ -233,13 +233,15 @@ __device__ __forceinline__ PrioEntry<TIER> prio_entry(const double *__restrict__
   const double *tab = table + (size_t)k * 2 * (B + 1);
   const double a = prof.a[k], w = prof.w[k];
   if constexpr (TIER == 0) {
-    // D2 = (C' - H') log2 e from the fp64 values, rounded once (NaN when both are -inf:
-    // prio_combine's clamp then gives -inf, the value of p = 0)
-    if (e == 0) return make_float4(-INFINITY, -INFINITY, NAN, 0.f);
+    // D2 = (C' - H') log2 e from the fp64 values, rounded once; +inf when H' = -inf
+    // (also when C' = -inf too: the y = 1 branch then returns lp = -inf, p = 0),
+    // so the exponent is never NaN and needs no clamp
+    if (e == 0) return make_float4(-INFINITY, -INFINITY, INFINITY, 0.f);
     const double C = tab[e - 1];
     const double Cr = C == -INFINITY ? -INFINITY : C - b * (a + w * (e - 1)) - b - lEL;
     const double Hr = e <= B ? tab[B + 1 + e] - lEL : -INFINITY;
-    return make_float4((float)Cr, (float)Hr, (float)((Cr - Hr) * 1.4426950408889634), 0.f);
+    const double D2 = Hr == -INFINITY ? INFINITY : (Cr - Hr) * 1.4426950408889634;
+    return make_float4((float)Cr, (float)Hr, (float)D2, 0.f);
   } else {
     if (e > B) return make_float2(-INFINITY, -INFINITY);  // unused pad
     const double C = tab[e];
@@ -272,10 +274,11 @@ struct PrioTabG {
 
 // The log-add-exp of TIER 0 with its exponent d2 = (lp - Hn) log2 e given:
 // log(e^lp + e^Hn g) = (d2 >= 0 ? lp : Hn) + log(1 + 2^-|d2| g  or  2^-|d2| + g)
-// (prio_combine with d2 from one FFMA of the table's D2; the same clamp).
+// (prio_combine with d2 from one FFMA of the table's D2, which is +inf
+// wherever Hn = -inf, so no clamp: 2^-inf = 0 after ftz).
 __device__ __forceinline__ float prio_combine_d2(float lp, float Hn, float d2, float g) {
-  const float e = ex2_approx(fmaxf(-fabsf(d2), -150.f));
-  const bool hi = !(d2 < 0.f);  // NaN (lp = Hn = -inf) -> hi: y = 1, lp = -inf
+  const float e = ex2_approx(-fabsf(d2));  // d2 is never NaN (the table's D2, prio_entry)
+  const bool hi = d2 >= 0.f;
   const float y = hi ? fmaf(e, g, 1.f) : e + g;
   return fmaf(0.6931471805599453f, lg2_approx(y), hi ? lp : Hn);
 }
