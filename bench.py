@@ -399,7 +399,9 @@ def main():
         "hbm_gbs_algorithmic": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "score_kernel<8,8,PICK,STREAM> (orloj_pick_batch)",
-                     "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
+                     "note": "the peak is a read+write copy; this kernel's bytes are >99.9 % reads (a read-only "
+                             "stream can run a little above the copy figure); traffic = ncu DRAM bytes per launch"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
