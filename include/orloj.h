@@ -422,7 +422,13 @@ orloj_status orloj_priority_table(const orloj_store *store, const orloj_latency_
                                   double *log_table, double *log_expected, void *stream);
 /* log p for every queue member and batch size: device float [num_sizes][N]
  * (size-major), N = queue_offsets[Q] - queue_offsets[0].  Uses only
- * queue_offsets, deadline_ticks and now_ticks.  Async on stream. */
+ * queue_offsets, deadline_ticks and now_ticks.  Async on stream.  The call
+ * re-bases the fp64 tables into an fp32 table per block and picks one of two
+ * arithmetic tiers on the host (a fitted polynomial for 1 - e^{-bx} when it
+ * holds to 2^-23 over the profile's bin widths, else a series / ex2 form);
+ * both meet |d log p| <= 1e-6 + 2^-22 |log p|.  A table
+ * larger than the shared-memory budget (num_sizes x (B+2) entries above
+ * ~88 KiB) is re-based into a stream-ordered scratch allocation instead. */
 orloj_status orloj_priority_scores(const orloj_store *store, const orloj_latency_profile *profile,
                                    int32_t num_sizes, double b_per_tick, const double *log_table,
                                    const double *log_expected, const orloj_queues *queues, float *log_priority,
