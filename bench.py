@@ -192,19 +192,43 @@ def oracle_c3_sample(cfg, nq: int, start: int = 0):
     return rows, local
 
 
-def time_oracle_c3(cfg, seconds: float, chunk: int = 64):
-    """Run the oracle on consecutive chunks of C3 queues until `seconds` of work."""
+def time_oracle_c3(cfg, seconds: float, chunk: int = 64, keep=None):
+    """Run the oracle on consecutive chunks of C3 queues until `seconds` of work.
+    keep: a list that receives (start, oracle result) per chunk (untimed use:
+    the bench's parity summary compares them with the GPU's k*)."""
     import oracle
     done, t_or, start = 0, 0.0, 0
     while t_or < seconds and start + chunk <= cfg.queues.Q:
         rows, local = oracle_c3_sample(cfg, chunk, start)
         t0 = time.perf_counter()
         F = oracle.cdf(rows)
-        oracle.score(F, cfg.profile.a, cfg.profile.w, local.offsets, local.deadline, local.dist, local.now)
+        res = oracle.score(F, cfg.profile.a, cfg.profile.w, local.offsets, local.deadline, local.dist, local.now)
         t_or += time.perf_counter() - t0
+        if keep is not None:
+            keep.append((start, res))
         done += chunk
         start += chunk
     return done, t_or, oracle.max_threads()
+
+
+def c3_parity_summary(kept, bk_gpu, kmax):
+    """k* of the GPU's timed C3 pick against the oracle on the cpu_baseline
+    sample: equal, or a difference within the E tolerance (a documented tie:
+    E_or[k_o] - E_or[k_g] <= 1e-5 (k_o + k_g)), else a mismatch."""
+    eq = tie = bad = 0
+    for start, res in kept:
+        ko = np.asarray(res["best_k"])
+        E = np.asarray(res["E"])
+        kg = bk_gpu[start:start + len(ko)]
+        for j in np.nonzero(kg != ko)[0]:
+            a, g = int(ko[j]), int(kg[j])
+            if g >= 1 and E[j, a - 1] - E[j, g - 1] <= 1e-5 * (a + g):
+                tie += 1
+            else:
+                bad += 1
+        eq += int((kg == ko).sum())
+    return {"queues": eq + tie + bad, "k_equal": eq, "k_documented_ties": tie, "k_mismatches": bad,
+            "source": "the cpu_baseline leg's fp64 oracle output on the same queues vs the timed GPU pick"}
 
 
 def time_oracle_configs(replay_scenarios: int = 256):
@@ -394,7 +418,8 @@ def main():
         "config": {"workload": WORKLOAD, "queues_per_gpu": Q, "requests_per_queue": int(np.diff(qn.offsets)[0]),
                    "bins": B, "kmax": cfg.kmax, "global_queues": world * Q,
                    "l2": "inputs larger than L2 (17.4 GB read per step); no flush",
-                   "parallelism": f"queues sharded, {world} independent C3 instances, no collective"},
+                   "parallelism": f"queues sharded, {world} independent C3 instances, no collective",
+                   "seed": gen.SEED_BASE + 3},
         "candidates_per_s": cand_s,
         "hbm_gbs_algorithmic": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -466,10 +491,12 @@ def main():
 
     # ---------------- cpu baseline (rank 0, N = 1 only) ----------------
     if world == 1 and not args.no_cpu_baseline:
-        n, secs, cores = time_oracle_c3(cfg, args.cpu_seconds)
+        kept = []
+        n, secs, cores = time_oracle_c3(cfg, args.cpu_seconds, keep=kept)
         result["cpu_baseline"] = {"value": n / secs, "unit": "decisions/s", "cores": cores, "kind": "oracle",
                                   "sample": f"first {n} C3 queues (256 x 256 bins, kmax 256), fp64 oracle, "
                                             f"{secs:.1f} s on {cores} host threads"}
+        result["parity"] = c3_parity_summary(kept, bk.cpu().numpy(), cfg.kmax)
         result["oracle_by_config"] = time_oracle_configs()
     else:
         result["cpu_baseline"] = None
