@@ -530,12 +530,13 @@ __device__ __forceinline__ void cx(uint32_t &ka, int &ia, uint32_t &kb, int &ib)
 // registers and the rest in shared memory; every round the lane holding the
 // best head (REDUX max over keys, then min over member indices among equal
 // keys) pops it and loads its next; round r's winner is kept by lane r.
-// Bitonic sort of one packed (key << 32 | ~member) per lane across the warp,
-// descending: rank r ends in lane r.  Packed keys are distinct (distinct
+// Bitonic sort of one packed (key << 32 | ~member) per lane across each group
+// of W lanes (W = 32: the warp), descending: rank r ends in lane r.  Packed keys are distinct (distinct
 // members), so one 64-bit compare orders (key desc, member asc).
+template <int W = 32>
 __device__ __forceinline__ uint64_t pop_bitonic32(uint64_t me, int lane) {
 #pragma unroll
-  for (int kk = 2; kk <= 32; kk <<= 1) {
+  for (int kk = 2; kk <= W; kk <<= 1) {
 #pragma unroll
     for (int j = kk >> 1; j > 0; j >>= 1) {
       const uint64_t p = __shfl_xor_sync(FULL, me, j);
@@ -602,7 +603,24 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
   const uint32_t hsel = __reduce_min_sync(FULL, kh > POP_KNEG ? kh : 0xffffffffu);
   const uint32_t mx2 = __reduce_max_sync(FULL, k2);
   if (mx2 < hsel && (mx2 <= POP_KNEG || __popc(__ballot_sync(FULL, kh > POP_KNEG)) >= bs)) {
-    const uint64_t me = pop_bitonic32(((uint64_t)kh << 32) | (uint32_t)~(32 * sh + lane), lane);
+    uint64_t me = ((uint64_t)kh << 32) | (uint32_t)~(32 * sh + lane);
+    // only the m selectable heads need ordering: with m <= 16 (m <= 8) they are
+    // compacted into lanes 0..m-1 through shared memory (the rest hold key 0)
+    // and a 16- (8-) lane network sorts them
+    const unsigned selb = __ballot_sync(FULL, kh > POP_KNEG);
+    const int m = __popc(selb);
+    if (m <= 16) {
+      uint2 *cmp = s_list[threadIdx.x >> 5][0];
+      cmp[lane] = make_uint2(0u, 0u);
+      __syncwarp();
+      if (kh > POP_KNEG) cmp[__popc(selb & ((1u << lane) - 1u))] = make_uint2((uint32_t)me, (uint32_t)(me >> 32));
+      __syncwarp();
+      const uint2 c = cmp[lane];
+      me = ((uint64_t)c.y << 32) | c.x;
+      me = m <= 8 ? pop_bitonic32<8>(me, lane) : pop_bitonic32<16>(me, lane);
+    } else {
+      me = pop_bitonic32<32>(me, lane);
+    }
     sel[q * 32 + lane] = (lane < bs && (uint32_t)(me >> 32) > POP_KNEG) ? (int)~(uint32_t)me : -1;
     return;
   }
