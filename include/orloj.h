@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define ORLOJ_ABI_VERSION 4
+#define ORLOJ_ABI_VERSION 5  /* 5: orloj_score_model.plan, orloj_score_model_prepare */
 #define ORLOJ_MAX_KMAX 256        /* candidate batch sizes per queue (score / pick) */
 #define ORLOJ_MAX_BINS 256        /* bins per histogram (score / pick) */
 #define ORLOJ_REPLAY_MAX_KMAX 32  /* window size in replay */

@@ -18,6 +18,8 @@ HEADER = os.path.join(ROOT, "include", "orloj.h")
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-shared", "-Xcompiler", "-fPIC"]
 
+ABI_VERSION = 5  # include/orloj.h ORLOJ_ABI_VERSION: the struct layouts below
+
 STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "COLD_START", 3: "UNSORTED", 4: "CAPACITY", 5: "CUDA", 6: "OOM"}
 
 
@@ -184,6 +186,9 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.orloj_abi_version() != ABI_VERSION:
+            raise OrlojError(1, f"{LIB_PATH} has ABI {L.orloj_abi_version()}, the binding expects {ABI_VERSION}: "
+                                "rebuild with __graft_entry__.build()")
         _lib = L
     return _lib
 

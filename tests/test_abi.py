@@ -33,7 +33,7 @@ def test_header_symbols_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.orloj_abi_version() == 4
+    assert lib.orloj_abi_version() == 5 == _abi.ABI_VERSION
 
 
 def test_sync_argument_errors(lib):
