@@ -175,10 +175,10 @@ orloj_status alloc_flag(unsigned int **dflag, cudaStream_t s) {
 // (G(0) = e^{-b} b / 2) on [0, U], the lowest degree D <= 5 that fits, by
 // interpolation at the D + 1 Chebyshev nodes (a Vandermonde solve in v = u / U, then c_k = q_k / U^k),
 // coefficients rounded to fp32.  Accepted when, on a grid of 257 points, the
-// fit holds to 2^-26 relative (fp64 coefficients) and to 2^-23 with the fp32
+// fit holds to 2^-23.5 relative (fp64 coefficients) and to 2^-22.5 with the fp32
 // coefficients (each rounded once: 2^-24 of its term), and u P(u) stays far
 // from the fp32 range for every |u| <= 2^31 (j = 0 rows: g finite).
-bool prio_fit_g(double b, double U, float *c) {
+bool prio_fit_g(double b, double U, float *c, int *degree) {
   constexpr int DMAX = 5;
   auto G = [&](double u) { return u > 0.0 ? std::exp(-b) * -std::expm1(-b * u / 2.0) / u : std::exp(-b) * b / 2.0; };
   // the lowest degree that fits (higher coefficients 0: no noise terms that
@@ -218,10 +218,11 @@ bool prio_fit_g(double b, double U, float *c) {
     bool ok = true;
     for (int i = 0; i <= 256 && ok; ++i) {
       const double u = U * i / 256.0;
-      ok = std::fabs(P(u, false) / G(u) - 1.0) <= std::ldexp(1.0, -26) &&  // the fit
-           std::fabs(P(u, true) / G(u) - 1.0) <= std::ldexp(1.0, -23);     // + fp32 coefficients
+      ok = std::fabs(P(u, false) / G(u) - 1.0) <= std::ldexp(1.0, -23.5) &&  // the fit
+           std::fabs(P(u, true) / G(u) - 1.0) <= std::ldexp(1.0, -22.5);     // + fp32 coefficients
     }
     if (!ok) continue;
+    *degree = D;
     double bound = 0.0;  // bounds |u P(u)| and every Horner partial times u for |u| <= 2^31
     for (int k = 0; k <= DMAX; ++k) bound += std::fabs((double)c[k]) * std::ldexp(1.0, 31 * (k + 1));
     return bound < 1e37;
@@ -254,10 +255,12 @@ cudaError_t prio_launch_tier(int tier, unsigned grid, size_t smem, cudaStream_t 
                              const double *log_expected, int32_t S, int32_t B, double b, const ProfileDev &prof,
                              const StepsDev &steps, const PrioCoef &cf, const orloj_queues *q, float *out,
                              const void *gtab) {
-  return tier == 0 ? prio_launch<SMEM_TABLE, STEPS, 0>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
-                                                        cf, q, out, gtab)
-                   : prio_launch<SMEM_TABLE, STEPS, 1>(grid, smem, s, log_table, log_expected, S, B, b, prof, steps,
-                                                        cf, q, out, gtab);
+  return tier == 0   ? prio_launch<SMEM_TABLE, STEPS, 0>(grid, smem, s, log_table, log_expected, S, B, b, prof,
+                                                          steps, cf, q, out, gtab)
+         : tier == 2 ? prio_launch<SMEM_TABLE, STEPS, 2>(grid, smem, s, log_table, log_expected, S, B, b, prof,
+                                                          steps, cf, q, out, gtab)
+                     : prio_launch<SMEM_TABLE, STEPS, 1>(grid, smem, s, log_table, log_expected, S, B, b, prof,
+                                                          steps, cf, q, out, gtab);
 }
 
 orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_profile *profile, int32_t S,
@@ -304,9 +307,10 @@ orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_
   for (int k = 0; k < S; ++k) wmax = prof.w[k] > wmax ? prof.w[k] : wmax;
   const int64_t cap0 = (1ll << 30) - 2 - wmax;
   PrioCoef cf;
-  bool t0 = b <= 0.05 && prio_fit_g(b, 2.0 * (wmax - 1), cf.c);
+  int deg = 5;
+  bool t0 = b <= 0.05 && prio_fit_g(b, 2.0 * (wmax - 1), cf.c, &deg);
   for (int k = 0; k < S && t0; ++k) t0 = (int64_t)prof.a[k] + (int64_t)prof.w[k] * B + 1 <= cap0;
-  const int tier = t0 ? 0 : 1;
+  const int tier = !t0 ? 1 : deg <= 4 ? 2 : 0;  // 0 / 2: fitted, degree 5 / <= 4
   cf.half_b = (float)(b / 2.0);
   cf.half_b_log2e = (float)(b / 2.0 * 1.4426950408889634);
   cf.gb = (float)(-std::expm1(-b));
@@ -321,7 +325,7 @@ orloj_status priority_scores_impl(const orloj_store *store, const orloj_latency_
     const int64_t ne = (int64_t)S * (B + 2);
     if (cudaMallocAsync(&gtab, (size_t)ne * PrioSmem::entry_bytes(tier), s) != cudaSuccess)
       return fail(ORLOJ_ERR_OOM, "priority_scores: cannot allocate the re-based table");
-    if (tier == 0)
+    if (tier != 1)  // the fitted tiers share one table layout
       priority_rebase_kernel<0><<<(unsigned)((ne + 255) / 256), 256, 0, s>>>(log_table, log_expected, S, B, b, prof,
                                                                             gtab);
     else

@@ -90,7 +90,7 @@ static __global__ void priority_table_kernel(const float *__restrict__ log2F, in
 // and with x > 0, i < B (x is then sigma - l1_{i+1} in (0, w)) the partial bin
 //   log p = log(e^{lp} + e^{H'} g),  g = 1 - e^{-b x}   (prio_combine, general g).
 //
-// TIER 0 (when the host's polynomial fit below holds to 2^-25 and every
+// TIERS 0 / 2 (when the host's polynomial fit below holds and every
 // horizon a_k + w_k B + 1 is under the tier's slack cap; the P1 case): a
 // strict-count lookup
 //   j = #bins with l2 < sigma, + 1   (= floor((sigma - 1 - a + w) / w) clamped to [0, B+1])
@@ -104,7 +104,9 @@ static __global__ void priority_table_kernel(const float *__restrict__ log2F, in
 // (g_b = 1 - e^{-b}, e_b = e^{-b}; both terms positive, no cancellation).  P is
 // a degree-5 polynomial fitted by the host (Chebyshev interpolation of
 // e_b (1 - e^{-b u/2}) / u on [0, 2 (max w - 1)], fp64, coefficients rounded
-// to fp32, then checked on a grid: 2^-26 relative for the fit, 2^-23 with the fp32 coefficients; else TIER 1).  j = 0
+// to fp32, then checked on a grid: 2^-23.5 relative for the fit, 2^-22.5 with the fp32 coefficients;
+// degree 5 is TIER 0, degree <= 4 TIER 2, no fit TIER 1; a relative error e in g
+// moves log p by at most e, 2^-22.5 = 1.7e-7 against the 1e-6 + 2^-22 |log p| budget).  j = 0
 // gives lp = Hn = -inf: prio_combine returns -inf (the host also checks that P
 // is finite for every u the cap allows).
 //
@@ -117,9 +119,11 @@ static __global__ void priority_table_kernel(const float *__restrict__ log2F, in
 // and PopBatch reads one size row coalesced).
 // Table entries: TIER 0 float4 {C', H', D2 = (C' - H') log2 e, 0} (the log-add-exp's
 // exponent in one FFMA), TIER 1 float2 {C', H'}.
-template <int TIER> using PrioEntry = typename std::conditional<TIER == 0, float4, float2>::type;
+// Tiers: 1 = general; 0 and 2 = the fitted-polynomial form (degree 5 and <= 4).
+__host__ __device__ constexpr bool prio_fitted(int tier) { return tier != 1; }
+template <int TIER> using PrioEntry = typename std::conditional<prio_fitted(TIER), float4, float2>::type;
 struct PrioSmem {
-  static __host__ __device__ size_t entry_bytes(int tier) { return tier == 0 ? 16 : 8; }
+  static __host__ __device__ size_t entry_bytes(int tier) { return prio_fitted(tier) ? 16 : 8; }
   static __host__ __device__ size_t table_bytes(int S, int B, int tier) { return (size_t)S * (B + 2) * entry_bytes(tier); }
   static __host__ __device__ size_t bytes(int S, int B, bool smem_table, int tier) {
     return (size_t)S * (16 + 8) + (smem_table ? table_bytes(S, B, tier) : 0);
@@ -219,7 +223,7 @@ __device__ __forceinline__ int32_t prio_s2(int64_t sigma, int32_t cap) {
 // sh}, nw2 = -2 w (TIER 0) or -w (TIER 1).
 template <int TIER>
 __device__ __forceinline__ int4 prio_lk(const ProfileDev &prof, int k, int B) {
-  return TIER == 0 ? make_int4(2 * (prof.a[k] + 1 - prof.w[k]), 2 * prof.w[k] * (B + 1), (int)prof.mag[k],
+  return prio_fitted(TIER) ? make_int4(2 * (prof.a[k] + 1 - prof.w[k]), 2 * prof.w[k] * (B + 1), (int)prof.mag[k],
                                (int)prof.sh[k])
                    : make_int4(prof.a2[k], prof.wB2[k], (int)prof.mag[k], (int)prof.sh[k]);
 }
@@ -232,7 +236,7 @@ __device__ __forceinline__ PrioEntry<TIER> prio_entry(const double *__restrict__
   const double lEL = logEL[k];
   const double *tab = table + (size_t)k * 2 * (B + 1);
   const double a = prof.a[k], w = prof.w[k];
-  if constexpr (TIER == 0) {
+  if constexpr (prio_fitted(TIER)) {
     // D2 = (C' - H') log2 e from the fp64 values, rounded once; +inf when H' = -inf
     // (also when C' = -inf too: the y = 1 branch then returns lp = -inf, p = 0),
     // so the exponent is never NaN and needs no clamp
@@ -293,12 +297,17 @@ __device__ __forceinline__ float prio_elem(const Tab &tk, const int4 &lk, int32_
   xc = xc > 0 ? xc : 0;
   const int j = (int)(__umulhi((uint32_t)xc, (uint32_t)lk.z) >> (uint32_t)lk.w);
   const PrioEntry<TIER> T = tk.template ld<PrioEntry<TIER>>(j);
-  if constexpr (TIER == 0) {
+  if constexpr (prio_fitted(TIER)) {
     const float u = (float)(x2 + nw * j);  // 2 (x - 1), x = sigma - l1_j
     const float lp = fmaf(-cf.half_b, u, T.x) - bxe;
     const float d2 = fmaf(-cf.half_b_log2e, u, T.z) - bxe * 1.4426950408889634f;  // (lp - Hn) log2 e
-    float c = fmaf(cf.c[5], u, cf.c[4]);
-    c = fmaf(c, u, cf.c[3]);
+    float c;
+    if constexpr (TIER == 0) {  // degree 5
+      c = fmaf(cf.c[5], u, cf.c[4]);
+      c = fmaf(c, u, cf.c[3]);
+    } else {  // degree <= 4 (TIER 2)
+      c = fmaf(cf.c[4], u, cf.c[3]);
+    }
     c = fmaf(c, u, cf.c[2]);
     c = fmaf(c, u, cf.c[1]);
     c = fmaf(c, u, cf.c[0]);
@@ -331,7 +340,7 @@ __global__ void PRIO_BOUNDS priority_scores_kernel(
   PrioEntry<TIER> *s_T = reinterpret_cast<PrioEntry<TIER> *>(s_wk + S);  // [S][B+2] (SMEM_TABLE)
   for (int k = threadIdx.x; k < S; k += blockDim.x) {
     s_lk[k] = prio_lk<TIER>(prof, k, B);
-    s_wk[k] = make_int2(TIER == 0 ? -2 * prof.w[k] : -prof.w[k], 0);
+    s_wk[k] = make_int2(prio_fitted(TIER) ? -2 * prof.w[k] : -prof.w[k], 0);
   }
   if (SMEM_TABLE)
     for (int e = threadIdx.x; e < S * (B + 2); e += blockDim.x) {

@@ -80,6 +80,9 @@ def test_scores_vs_oracle(name, b_scale):
     assert (np.isneginf(got) == ninf).all(), int((np.isneginf(got) != ninf).sum())
     err = np.abs(got[~ninf] - ref[~ninf])
     assert (err <= _tol(ref[~ninf])).all(), float(err.max())
+    import _parity as par
+    par.record("priority_tolerance_use", label=f"{name}/b{b_scale}",
+               max_err_over_tol=float((err / _tol(ref[~ninf])).max()), max_abs_err=float(err.max()))
     exact = pr.scores(fam.counts, prof.a, prof.w, S, b, q.offsets, q.deadline, q.now, weights)
     assert ((exact == -np.inf) == ninf).all()
     # against the paper's Eq. 2 on the real (exact-count) histograms: the GPU
