@@ -59,12 +59,15 @@ def parse():
     ap.add_argument("--replay-seeds", type=int, default=256, help="seeds per (family, bucket)")
     ap.add_argument("--replay-arrivals", type=int, default=100_000)
     ap.add_argument("--replay-reps", type=int, default=2)
-    ap.add_argument("--replay-segments", default="auto",
-                    help="segments per scenario of the segmented replay ('auto' or an int; 1 = plain kernel)")
+    ap.add_argument("--replay-segments", default="auto,last=x2",
+                    help="segments per scenario of the segmented replay ('auto' or an int; 1 = plain kernel; "
+                         "'fam=G' per family; 'last=G' / 'last=xM' for the family launched last)")
     ap.add_argument("--seg-sweep-n", default="1,2,4,8")
     ap.add_argument("--seg-sweep-g", default="1,2,4,8,16,32,64,auto")
     ap.add_argument("--replay-seg-sweep", action="store_true",
                     help="diagnostic: time the C5 sweep and its rank-0 shards for several segment counts")
+    ap.add_argument("--scenario-order", default="seed", choices=["seed", "bucket"],
+                    help="order of a rank's C5 scenarios in its trace (seed groups, or SLO bucket by bucket)")
     ap.add_argument("--no-shard-proxy", action="store_true")
     ap.add_argument("--proxy-segments", default=None, help="segments per scenario in the shard proxy (default: as --replay-segments)")
     ap.add_argument("--no-policies", action="store_true", help="skip the replay policy-variant sweep")
@@ -842,6 +845,12 @@ def build_replay(args, rank, world, dev):
     nb = len(gen.BUCKET_SLO_MULTS)
     u = np.arange(nb * args.replay_seeds)
     mine = parallel.shard_round_robin(u // nb, rank, world)    # seed groups round-robin over ranks
+    if getattr(args, "scenario_order", "seed") == "bucket":
+        # the trace lists a rank's scenarios bucket by bucket: a block's warps then
+        # replay scenarios of one SLO bucket (similar lengths), so fewer warp slots
+        # idle while a block's slowest warp finishes (the counters are per bucket,
+        # so the order changes nothing else)
+        mine = mine[np.argsort(mine % nb, kind="stable")]
     return [wl.C5Family(name, local_ids=mine, n_arr=args.replay_arrivals, seeds_per_bucket=args.replay_seeds,
                         device=dev) for name in gen.C5_FAMILIES]
 
@@ -856,11 +865,23 @@ def family_segments(spec, name: str):
     for part in spec.split(","):
         if "=" in part:
             k, v = part.split("=", 1)
+            if k.strip() == "last":    # time_replay: the family launched last
+                continue
             if k.strip() == name:
                 return v.strip()
         elif part.strip():
             default = part.strip()
     return default
+
+
+def last_segments(spec, g: int) -> int:
+    """Segments of the family launched last: "last=G" in the spec (an int, or
+    "xM" for M times its own count), else its own count g."""
+    for part in str(spec).split(","):
+        if "=" in part and part.split("=", 1)[0].strip() == "last":
+            v = part.split("=", 1)[1].strip()
+            return max(1, g * int(v[1:])) if v.startswith("x") else max(1, int(v))
+    return g
 
 
 def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
@@ -951,6 +972,18 @@ def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True, segments=
         lo, hi = torch.cuda.Stream.priority_range()       # (lowest, highest); numerically hi <= lo
         rank_of = {i: r for r, i in enumerate(order)}
         streams = [torch.cuda.Stream(dev, priority=min(lo, hi + rank_of[i])) for i in range(len(fams))]
+        # The families run nearly one after another (stream priorities); the
+        # sweep ends when the last family's first pass drains, which takes about
+        # one of its items' duration.  "last=G" gives that family G segments
+        # (shorter items) — chosen after the order is known, then re-warmed.
+        lastg = last_segments(segments, segs[order[-1]])
+        if lastg != segs[order[-1]]:
+            i = order[-1]
+            segs[i] = lastg
+            wss[i] = torch.empty(max(orj.replay_seg_workspace_bytes(fams[i].trace, lastg), 1), dtype=torch.uint8,
+                                 device=dev)
+            once()
+            torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
@@ -984,7 +1017,8 @@ def run_policies(args, rank, world, dev):
         f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).to(dev) for f in fams}
     nb = len(gen.BUCKET_SLO_MULTS)
     # segmented replay (same counters as the plain kernel, bit for bit), workspaces outside the timing
-    segs = [replay_segments(args.replay_segments, f.trace.num_scenarios, args.replay_arrivals) for f in fams]
+    segs = [replay_segments(family_segments(args.replay_segments, f.tf.fam.name), f.trace.num_scenarios,
+                            args.replay_arrivals) for f in fams]
     wss = {f.tf.fam.name: torch.empty(max(orj.replay_seg_workspace_bytes(f.trace, g), 1), dtype=torch.uint8,
                                       device=dev) for f, g in zip(fams, segs)}
     out = {"sweep": f"4 families x 8 buckets x {seeds} seeds x {args.replay_arrivals} arrivals",
@@ -1052,7 +1086,8 @@ def run_b_sweep(args, rank, world, dev):
     a2.replay_seeds = args.policy_seeds
     fams = build_replay(a2, rank, world, dev)
     nb = len(gen.BUCKET_SLO_MULTS)
-    segs = [replay_segments(args.replay_segments, f.trace.num_scenarios, args.replay_arrivals) for f in fams]
+    segs = [replay_segments(family_segments(args.replay_segments, f.tf.fam.name), f.trace.num_scenarios,
+                            args.replay_arrivals) for f in fams]
     wss = [torch.empty(max(orj.replay_seg_workspace_bytes(f.trace, g), 1), dtype=torch.uint8, device=dev)
            for f, g in zip(fams, segs)]
     thr = [torch.from_numpy(policy.alg1_size_thresholds(f.tf.fam.counts, f.tf.profile.a, f.tf.profile.w)).to(dev)

@@ -110,7 +110,23 @@ struct ReplaySeg {
   SegRec ext[SEG_REC];  // its extension past the end state (marks from s_{g+1}; running counters)
   int64_t carry_D[32], carry_h[32];
   int32_t carry_d[32], carry_tb[32];
+#ifdef ORLOJ_REPLAY_TIMELINE  // diagnostic builds: %globaltimer at the item's start / end, SM id
+  long long tl[4];            // first pass start / end; (segment 0 only) stitch start / end
+  int32_t tl_sm[2], tl_pad[2];
+#endif
 };
+#ifdef ORLOJ_REPLAY_TIMELINE
+__device__ __forceinline__ long long tl_now() {
+  long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+__device__ __forceinline__ int tl_smid() {
+  int v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+#endif
 
 // first arrival of segment g of G over n arrivals: floor(g n / G) without overflow
 __host__ __device__ inline int64_t seg_begin(int64_t n, int g, int G) {
@@ -248,8 +264,8 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   int g = 0;  // MODE 1: this warp's segment; MODE 2: the segment being stitched
   if constexpr (MODE == 1) {
     if (u >= p.S * p.G) return;
-    s = u / p.G;
-    g = (int)(u - s * p.G);
+    g = (int)(u / p.S);  // segment-major items: a block's warps replay the same segment of 4 scenarios
+    s = u - (int64_t)g * p.S;
   } else {
     if (s >= p.S) return;
   }
@@ -303,7 +319,13 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
     __syncwarp();
     if (g + 1 < p.G) seg_end = (int32_t)seg_begin(n, g + 1, p.G);
-    sg = opaque_ptr(p.seg + u);  // used only in the (cold) segment hooks
+    sg = opaque_ptr(p.seg + s * p.G + g);  // used only in the (cold) segment hooks
+#ifdef ORLOJ_REPLAY_TIMELINE
+    if (lane == 0) {
+      sg->tl[0] = tl_now();
+      sg->tl_sm[0] = tl_smid();
+    }
+#endif
     if (g > 0) mylog = p.seg_log ? p.seg_log + seg_log_off(base, s, n, g, p.G) : nullptr;
   }
   // window slots start as valid entries (distribution 0, bin 1): the scoring
@@ -419,6 +441,12 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
   if constexpr (MODE == 2) {
     // segment 0 ran from the true start: the true run is at its end state
     sg = opaque_ptr(p.seg + s * p.G);
+#ifdef ORLOJ_REPLAY_TIMELINE
+    if (lane == 0) {
+      sg->tl[2] = tl_now();
+      sg->tl_sm[1] = tl_smid();
+    }
+#endif
     ndec = (int32_t)sg[0].ndec;  // segment 0 wrote its decisions into the true log
     taken = ndec;
     c_fin = (uint32_t)sg[0].ctr[0];
@@ -858,11 +886,17 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     if (lane == 0) {
       sg->next = ext ? nrec : 0;
       if (ext) atomicAdd(p.seg_stats + 3, (unsigned long long)(ndec - sg->ndec));
+#ifdef ORLOJ_REPLAY_TIMELINE
+      sg->tl[1] = tl_now();
+#endif
     }
     return;
   }
   if constexpr (MODE == 2) {
     if (lane == 0) {
+#ifdef ORLOJ_REPLAY_TIMELINE
+      p.seg[s * p.G].tl[3] = tl_now();
+#endif
       atomicAdd(p.seg_stats + 0, (unsigned long long)(ndec - taken));
       atomicAdd(p.seg_stats + 1, (unsigned long long)joined);
       atomicAdd(p.seg_stats + 2, (unsigned long long)crossed);
