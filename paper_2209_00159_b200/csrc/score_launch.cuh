@@ -58,7 +58,7 @@ cudaError_t launch_score_small(const ScoreParams &p, cudaStream_t s) {
   const int64_t blocks = (p.Q + SMALL_WARPS - 1) / SMALL_WARPS;
   const size_t smem = SmallShape<BPL>::bytes(p.D, p.B);
   static std::atomic<uint64_t> configured{0};
-  const size_t cap = SmallShape<BPL>::bytes((int)(SMEM_STORE_BYTES / (32 * BPL * 4)), 32 * BPL);
+  const size_t cap = (size_t)SMEM_STORE_BYTES;
   cudaError_t e = ensure_max_dyn_smem(score_small_kernel<BPL, PICK>, (int)cap, configured);
   if (e != cudaSuccess) return e;
   score_small_kernel<BPL, PICK><<<(unsigned)blocks, SMALL_WARPS * 32, smem, s>>>(p);
