@@ -898,8 +898,12 @@ def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
 REPLAY_LAUNCHES = os.path.join(ROOT, "profiles", "replay_sweep_launches.csv")
 
 
+REPLAY_SWEEP_SEGS = [8, 8, 8, 16]   # the default sweep: 8 segments, 16 for the family launched last
+
+
 def replay_sweep_instructions():
-    """Warp instructions of one full 1-GPU C5 sweep at 8 segments: the sum of
+    """Warp instructions of one full 1-GPU C5 sweep at the default segments
+    (REPLAY_SWEEP_SEGS): the sum of
     smsp__inst_executed.sum over the last sweep's launches in the committed
     ncu launch list (profiles/replay_sweep_launches.csv, re-captured with
     scripts/gpu_replay_check.sh whenever the replay kernel changes).  The
@@ -1195,7 +1199,7 @@ def run_replay(args, rank, world, dev, barrier, max_over_ranks):
            "collective": "one torch.distributed.all_reduce of the int64 [4 x 8 x 7] counters (NCCL) per sweep, "
                          "inside the timed region"}
     instr = replay_sweep_instructions()
-    if (world == 1 and segs == [8, 8, 8, 8] and args.replay_seeds == 256
+    if (world == 1 and sorted(segs) == REPLAY_SWEEP_SEGS and args.replay_seeds == 256
             and args.replay_arrivals == 100_000 and instr):
         # issue roofline of the full 1-GPU sweep: the warp-instruction count is a
         # property of the (deterministic) workload and the code, counted by ncu

@@ -6,15 +6,18 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-cur_file, hdr, agg, fn_seen = None, None, [], 0
+cur_file, hdr, agg, fn_seen, first_fn = None, None, [], 0, None
 for r in rows:
     if not r:
         continue
     if r[0] == "File Path":
         cur_file = r[1].split("/")[-1]
         continue
-    if r[0] == "Function Name":
-        fn_seen += 1
+    if r[0] == "Function Name":  # one row per source file; stop at the next kernel
+        if fn_seen and r[1] != first_fn:
+            fn_seen = 2
+        else:
+            fn_seen, first_fn = 1, r[1]
         continue
     if r[0] == "Line No":
         hdr = r
