@@ -487,6 +487,10 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
     }
   };
   const int64_t a1 = p.prof.a[0], w1 = p.prof.w[0];
+  // the max-plus scan runs on 32-bit offsets from the first lookahead arrival
+  // when 32 batch durations (each <= a_1 + w_1 B) and the lookahead's arrival
+  // offsets stay below 2^29 (exact: every value below 2^30 + 2^29, no wrap)
+  const bool scan32 = 32 * (a1 + w1 * (int64_t)B) < (1ll << 29);
 
   while (cursor < ni || ncarry > 0) {
     if constexpr (MODE == 1) {
@@ -575,15 +579,34 @@ replay_kernel(const __grid_constant__ ReplayParams p) {
       const bool ok0 = __ballot_sync(FULL, lane == 0 && va && an > t0 && t0 <= hj) != 0u;
       if (ok0) {  // warp-uniform
         const int64_t dj = a1 + w1 * ut;
-        int64_t P = va ? dj : 0, Qv = va ? ua + dj : INT64_MIN;
+        int64_t P, Qv;
+        const int64_t base = __shfl_sync(FULL, ua, 0);  // lane 0 is a real arrival (ok0)
+        if (scan32 && __all_sync(FULL, !va || ua - base < (1ll << 29))) {
+          // the same scan on 32-bit offsets (values equal to the 64-bit scan's)
+          int32_t P32 = va ? (int32_t)dj : 0, Q32 = va ? (int32_t)(ua - base) + (int32_t)dj : INT32_MIN;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int64_t Pp = __shfl_up_sync(FULL, P, off);
-          const int64_t Qp = __shfl_up_sync(FULL, Qv, off);
-          if (lane >= off) {
-            const int64_t q2 = Qp + P;
-            Qv = q2 > Qv ? q2 : Qv;
-            P += Pp;
+          for (int off = 1; off < 32; off <<= 1) {
+            const int32_t Pp = __shfl_up_sync(FULL, P32, off);
+            const int32_t Qp = __shfl_up_sync(FULL, Q32, off);
+            if (lane >= off) {
+              Q32 = max(Qp + P32, Q32);
+              P32 += Pp;
+            }
+          }
+          P = P32;
+          Qv = base + Q32;  // >= base + Q of lane 0: a real value in every lane
+        } else {
+          P = va ? dj : 0;
+          Qv = va ? ua + dj : INT64_MIN;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int64_t Pp = __shfl_up_sync(FULL, P, off);
+            const int64_t Qp = __shfl_up_sync(FULL, Qv, off);
+            if (lane >= off) {
+              const int64_t q2 = Qp + P;
+              Qv = q2 > Qv ? q2 : Qv;
+              P += Pp;
+            }
           }
         }
         const int64_t Tj = t + P > Qv ? t + P : Qv;  // t may be INT64_MIN: t + P does not overflow
