@@ -25,4 +25,5 @@ SKIP_TESTS=1 bash scripts/gpu_priority_prof.sh
 timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active \
   --clock-control none --csv -k regex:model --log-file gpurun_out/model_launches.csv python scripts/model_variants_prof.py > gpurun_out/ncu_model.log 2>&1
 python scripts/model_instr.py gpurun_out/model_launches.csv gpurun_out/model_variants_instr.json > gpurun_out/model_instr.log 2>&1
+ORLOJ_BENCH_SHARE_GPU=1 timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 > gpurun_out/bench_n2_shared.log 2>&1; echo "n2 rc=$?" >> gpurun_out/bench_n2_shared.log
 echo done > gpurun_out/final_done.txt

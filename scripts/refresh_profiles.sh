@@ -25,4 +25,5 @@ if [ -f gpurun_out/model_variants_instr.json ]; then
   sed 's#"source": "gpurun_out/model_launches.csv"#"source": "ncu launch list of scripts/model_variants_prof.py (scripts/gpu_round2_final.sh)"#' \
     gpurun_out/model_variants_instr.json > profiles/model_variants_instr.json
 fi
+[ -f gpurun_out/bench_n2_shared.log ] && cp gpurun_out/bench_n2_shared.log profiles/r02_bench_n2_shared_gpu_functional.log
 echo refreshed

@@ -139,3 +139,36 @@ def test_replay_determinism():
         torch.cuda.synchronize()
         logs.append((pb.cpu().numpy(), log.cpu().numpy()))
     assert (logs[0][0] == logs[1][0]).all() and (logs[0][1] == logs[1][1]).all()
+
+
+@pytest.mark.parametrize("scale", [1, 256, 2048])
+def test_replay_time_scale_scan_paths(scale):
+    """Every time scaled by c (arrivals, SLOs, a_k, w_k): the same decisions.
+    c = 2048 puts 32 durations above 2^29, so every max-plus run scan takes the
+    64-bit path; c = 256 keeps the 32-bit path except where a lookahead spans
+    2^29 ticks; c = 1 is the 32-bit path throughout.  Static family: integer
+    E_k, so the GPU equals the oracle's free run exactly, and the decision log
+    is the unscaled one."""
+    tf = gen.c5_trace_family("static")
+    gids, bucket, slo = gen.c5_scenarios(tf, 2)
+    n = 5000
+    arr, dist, tb = gen.trace_host(tf, gids, n)
+    off = np.arange(len(gids) + 1, dtype=np.int64) * n
+    a = tf.profile.a.astype(np.int64) * scale
+    w = tf.profile.w.astype(np.int64) * scale
+    assert int(a[-1]) + int(w[-1]) * tf.fam.B < (1 << 30)            # within the validated horizon
+    if scale == 2048:
+        assert 32 * (int(a[0]) + int(w[0]) * tf.fam.B) >= (1 << 29)  # the kernel's 64-bit scan
+    store = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks * scale)
+    prof = orj.LatencyProfile(a, w)
+    t0 = arr.reshape(len(gids), n)[:, :1]
+    arr_s = (t0 + (arr.reshape(len(gids), n) - t0) * scale).reshape(-1)  # scaled about each scenario's start
+    pb, log = _gpu_replay(store, prof, off, arr_s, dist, tb, slo * scale)  # one counter row per scenario
+    F = oracle.cdf(tf.fam.counts)
+    free = oracle.replay(F, a, w, off, arr_s, dist, tb, slo * scale, want_log=True)
+    assert (free["counters"] == pb).all()
+    assert (free["log"] == log).all()
+    if scale != 1:
+        store1 = orj.HistogramStore.from_counts(tf.fam.counts, tf.fam.bin_ticks)
+        _, log1 = _gpu_replay(store1, orj.LatencyProfile(tf.profile.a, tf.profile.w), off, arr, dist, tb, slo)
+        assert (log1 == log).all()
