@@ -619,7 +619,7 @@ orloj_status orloj_pop_batch(const orloj_queues *queues, const float *logp, int3
   if (S < 1) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pop_batch: num_sizes < 1");
   if (queues->num_queues == 0) return ok();
   if (!logp || !bs || !sel) return fail(ORLOJ_ERR_INVALID_ARGUMENT, "pop_batch: NULL array");
-  const int64_t threads = queues->num_queues * 32;
+  const int64_t threads = (queues->num_queues + POP_QPW - 1) / POP_QPW * 32;  // POP_QPW queues per warp
   pop_batch_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       logp, S, queues->num_queues, queues->queue_offsets, bs, sel);
   const cudaError_t e = cudaGetLastError();

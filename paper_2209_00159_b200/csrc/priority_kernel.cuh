@@ -562,34 +562,10 @@ __device__ __forceinline__ uint64_t pop_bitonic32(uint64_t me, int lane) {
 // the queue end hold 0.
 constexpr uint32_t POP_KNEG = 0x007fffffu;
 
-static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__restrict__ logp, int32_t S, int64_t Q,
-                                                               const int64_t *__restrict__ offsets,
-                                                               const int32_t *__restrict__ bs_q,
-                                                               int32_t *__restrict__ sel) {
-  __shared__ uint2 s_list[8][9][32];  // per warp: sorted (key, id) positions 1..7 of each lane, 8 = sentinel
-  const int lane = threadIdx.x & 31;
-  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (q >= Q) return;
-  const int64_t base0 = offsets[0];
-  const int64_t b0 = offsets[q] - base0, N = offsets[Q] - base0;
-  const int n = (int)(offsets[q + 1] - offsets[q]);
-  int bs = bs_q[q];
-  bs = (bs >= 1 && bs <= S) ? bs : 0;
-  if (n <= 0 || !bs) {  // nothing selectable (warp-uniform)
-    sel[q * 32 + lane] = -1;
-    return;
-  }
-  // all 8 loads first and unconditional, so they are in flight together (a
-  // short queue's lanes past the end re-read its last member, masked below)
-  const float *row = logp + (int64_t)(bs - 1) * N + b0;
-  float v[8];
-  if (n >= 256) {
-#pragma unroll
-    for (int s = 0; s < 8; ++s) v[s] = __ldg(row + 32 * s + lane);
-  } else {
-#pragma unroll
-    for (int s = 0; s < 8; ++s) v[s] = __ldg(row + min(32 * s + lane, n - 1));
-  }
+// One queue of PopBatch: v[s] = log-priority of member 32 s + lane (any value
+// past the queue end, masked by n), bs in 1..S; lst: this warp's shared lists.
+__device__ __forceinline__ void pop_one(const float (&v)[8], int n, int bs, int lane, uint2 (*lst)[32],
+                                        int32_t *__restrict__ out) {
   uint32_t k[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
@@ -619,7 +595,7 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
     const unsigned selb = __ballot_sync(FULL, kh > POP_KNEG);
     const int m = __popc(selb);
     if (m <= 16) {
-      uint2 *cmp = s_list[threadIdx.x >> 5][0];
+      uint2 *cmp = lst[0];
       cmp[lane] = make_uint2(0u, 0u);
       __syncwarp();
       if (kh > POP_KNEG) cmp[__popc(selb & ((1u << lane) - 1u))] = make_uint2((uint32_t)me, (uint32_t)(me >> 32));
@@ -630,7 +606,7 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
     } else {
       me = pop_bitonic32<32>(me, lane);
     }
-    sel[q * 32 + lane] = (lane < bs && (uint32_t)(me >> 32) > POP_KNEG) ? (int)~(uint32_t)me : -1;
+    out[lane] = (lane < bs && (uint32_t)(me >> 32) > POP_KNEG) ? (int)~(uint32_t)me : -1;
     return;
   }
   int id[8];
@@ -643,8 +619,7 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
   cx(k[0], id[0], k[4], id[4]); cx(k[1], id[1], k[5], id[5]); cx(k[2], id[2], k[6], id[6]); cx(k[3], id[3], k[7], id[7]);
   cx(k[2], id[2], k[4], id[4]); cx(k[3], id[3], k[5], id[5]);
   cx(k[1], id[1], k[2], id[2]); cx(k[3], id[3], k[4], id[4]); cx(k[5], id[5], k[6], id[6]);
-  uint2(*lst)[32] = s_list[threadIdx.x >> 5];
-#pragma unroll
+  #pragma unroll
   for (int s = 1; s < 8; ++s) lst[s][lane] = make_uint2(k[s], (uint32_t)id[s]);
   lst[8][lane] = make_uint2(0u, 0x7fffffffu);
   __syncwarp();
@@ -662,7 +637,68 @@ static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__re
       hid = (int)nx.y;
     }
   }
-  sel[q * 32 + lane] = mine;
+  out[lane] = mine;
+}
+
+// QPW queues per warp: every queue's offsets and all QPW x 8 member loads are
+// issued before the first queue is processed, so the loads of the later queues
+// are in flight while the earlier ones sort (ORLOJ_POP_QPW; 1 = one queue per warp).
+#ifndef ORLOJ_POP_QPW
+#define ORLOJ_POP_QPW 2
+#endif
+constexpr int POP_QPW = ORLOJ_POP_QPW;
+static __global__ void __launch_bounds__(256) pop_batch_kernel(const float *__restrict__ logp, int32_t S, int64_t Q,
+                                                               const int64_t *__restrict__ offsets,
+                                                               const int32_t *__restrict__ bs_q,
+                                                               int32_t *__restrict__ sel) {
+  __shared__ uint2 s_list[8][9][32];  // per warp: sorted (key, id) positions 1..7 of each lane, 8 = sentinel
+  const int lane = threadIdx.x & 31;
+  const int64_t q0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * POP_QPW;
+  if (q0 >= Q) return;
+  const int64_t base0 = offsets[0], N = offsets[Q] - base0;
+  int64_t b0[POP_QPW];
+  int n[POP_QPW], bs[POP_QPW];
+#pragma unroll
+  for (int j = 0; j < POP_QPW; ++j) {
+    const int64_t q = q0 + j;
+    b0[j] = 0;
+    n[j] = 0;
+    bs[j] = 0;
+    if (q < Q) {
+      b0[j] = offsets[q] - base0;
+      n[j] = (int)(offsets[q + 1] - offsets[q]);
+      const int b = bs_q[q];
+      bs[j] = (b >= 1 && b <= S) ? b : 0;
+    }
+  }
+  // all loads first and unconditional within a queue, so they are in flight
+  // together (a short queue's lanes past the end re-read its last member,
+  // masked later)
+  float v[POP_QPW][8];
+#pragma unroll
+  for (int j = 0; j < POP_QPW; ++j) {
+    if (n[j] <= 0 || !bs[j]) continue;  // nothing selectable (warp-uniform)
+    const float *row = logp + (int64_t)(bs[j] - 1) * N + b0[j];
+    if (n[j] >= 256) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) v[j][s] = __ldg(row + 32 * s + lane);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) v[j][s] = __ldg(row + min(32 * s + lane, n[j] - 1));
+    }
+  }
+  uint2(*lst)[32] = s_list[threadIdx.x >> 5];
+#pragma unroll
+  for (int j = 0; j < POP_QPW; ++j) {
+    if (q0 + j >= Q) break;
+    int32_t *out = sel + (q0 + j) * 32;
+    if (n[j] <= 0 || !bs[j]) {
+      out[lane] = -1;
+      continue;
+    }
+    if (j > 0) __syncwarp();  // the previous queue's list reads are done
+    pop_one(v[j], n[j], bs[j], lane, lst, out);
+  }
 }
 
 }  // namespace orloj

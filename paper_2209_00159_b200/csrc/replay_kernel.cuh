@@ -142,7 +142,10 @@ __host__ __device__ inline int64_t seg_log_off(int64_t arr_off_s, int64_t s, int
   return 2 * arr_off_s + seg_begin(n, g, G) + seg_begin(n, g + 1, G) - seg_begin(n, 1, G) + (s * G + g) * 34;
 }
 
-constexpr int REPLAY_WARPS = 4;
+#ifndef ORLOJ_REPLAY_WARPS
+#define ORLOJ_REPLAY_WARPS 4
+#endif
+constexpr int REPLAY_WARPS = ORLOJ_REPLAY_WARPS;  // warps (scenarios / segments) per CTA
 // ORLOJ_REPLAY_STATS (diagnostic variant builds only): MODE 1 adds per-decision
 // statistics to the workspace head: [5] decisions committed by the max-plus
 // run path, [6] scanned decisions with a carried window, [7 + wc] windows of

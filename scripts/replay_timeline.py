@@ -25,7 +25,8 @@ def main():
     world, r = int(os.environ.get("WORLD", "8")), int(os.environ.get("RANK_", "0"))
     fams = bench.build_replay(args, r, world, dev)
     names = [f.tf.fam.name for f in fams]
-    segs = [bench.replay_segments(os.environ.get("SEGS", "auto"), f.trace.num_scenarios,
+    spec = os.environ.get("SEGS", "auto,last=x2")
+    segs = [bench.replay_segments(bench.family_segments(spec, f.tf.fam.name), f.trace.num_scenarios,
                                   f.trace.num_arrivals // max(f.trace.num_scenarios, 1)) for f in fams]
     wss = [torch.empty(orj.replay_seg_workspace_bytes(f.trace, g), dtype=torch.uint8, device=dev)
            for f, g in zip(fams, segs)]
@@ -49,6 +50,10 @@ def main():
             order = sorted(range(len(fams)), key=lambda i: -work[i])
             rank_of = {i: k for k, i in enumerate(order)}
             streams = [torch.cuda.Stream(dev, priority=min(lo, hi + rank_of[i])) for i in range(len(fams))]
+            i = order[-1]
+            segs[i] = bench.last_segments(spec, segs[i])   # as the bench: the family launched last
+            wss[i] = torch.empty(orj.replay_seg_workspace_bytes(fams[i].trace, segs[i]), dtype=torch.uint8,
+                                 device=dev)
             continue
         out[f"rep{rep}_ms_end"] = {names[i]: round(start.elapsed_time(ends[i]), 3) for i in range(len(fams))}
     spans = {}
