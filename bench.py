@@ -59,9 +59,9 @@ def parse():
     ap.add_argument("--replay-seeds", type=int, default=256, help="seeds per (family, bucket)")
     ap.add_argument("--replay-arrivals", type=int, default=100_000)
     ap.add_argument("--replay-reps", type=int, default=2)
-    ap.add_argument("--replay-segments", default="auto,last=x2",
+    ap.add_argument("--replay-segments", default="auto,last=auto",
                     help="segments per scenario of the segmented replay ('auto' or an int; 1 = plain kernel; "
-                         "'fam=G' per family; 'last=G' / 'last=xM' for the family launched last)")
+                         "'fam=G' per family; 'last=G' / 'last=xM' / 'last=auto' for the family launched last)")
     ap.add_argument("--seg-sweep-n", default="1,2,4,8")
     ap.add_argument("--seg-sweep-g", default="1,2,4,8,16,32,64,auto")
     ap.add_argument("--replay-seg-sweep", action="store_true",
@@ -874,24 +874,28 @@ def family_segments(spec, name: str):
     return default
 
 
-def last_segments(spec, g: int) -> int:
-    """Segments of the family launched last: "last=G" in the spec (an int, or
-    "xM" for M times its own count), else its own count g."""
+def last_segments(spec, g: int, n_scen_family: int) -> int:
+    """Segments of the family launched last: "last=G", "last=xM" (M times its
+    own count) or "last=auto" in the spec, else its own count g.  "auto": 2x
+    while the family has >= 2,048 scenarios on the rank (one GPU), else 4x
+    (the shard sweeps of DESIGN.md §12: the last family's items set the drain)."""
     for part in str(spec).split(","):
         if "=" in part and part.split("=", 1)[0].strip() == "last":
             v = part.split("=", 1)[1].strip()
+            if v == "auto":
+                return g * (2 if n_scen_family >= 2048 else 4)
             return max(1, g * int(v[1:])) if v.startswith("x") else max(1, int(v))
     return g
 
 
 def replay_segments(spec, n_scen_family: int, n_arr: int) -> int:
     """Segments per scenario for the segmented replay.  "auto": 8 per scenario
-    while a family has >= 1,024 scenarios on this rank, 16 from 512, else 24
-    (the C5 sweep's measured optimum at 1/2/4/8-GPU shard sizes),
-    never below ~2,000 arrivals per segment."""
+    while a family has >= 2,048 scenarios on this rank (the 1-GPU sweep), else 12
+    (the 2/4/8-GPU shards; with the last family at 4x: DESIGN.md §12), never
+    below ~2,000 arrivals per segment."""
     if spec != "auto":
         return max(1, int(spec))
-    g = 8 if n_scen_family >= 1024 else 16 if n_scen_family >= 512 else 24
+    g = 8 if n_scen_family >= 2048 else 12
     return int(max(1, min(g, n_arr // 2000, 4096)))
 
 
@@ -980,7 +984,7 @@ def time_replay(fams, reps, dev, barrier, max_over_ranks, reduce=True, segments=
         # sweep ends when the last family's first pass drains, which takes about
         # one of its items' duration.  "last=G" gives that family G segments
         # (shorter items) — chosen after the order is known, then re-warmed.
-        lastg = last_segments(segments, segs[order[-1]])
+        lastg = last_segments(segments, segs[order[-1]], fams[order[-1]].trace.num_scenarios)
         if lastg != segs[order[-1]]:
             i = order[-1]
             segs[i] = lastg

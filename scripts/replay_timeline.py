@@ -25,7 +25,7 @@ def main():
     world, r = int(os.environ.get("WORLD", "8")), int(os.environ.get("RANK_", "0"))
     fams = bench.build_replay(args, r, world, dev)
     names = [f.tf.fam.name for f in fams]
-    spec = os.environ.get("SEGS", "auto,last=x2")
+    spec = os.environ.get("SEGS", "auto,last=auto")
     segs = [bench.replay_segments(bench.family_segments(spec, f.tf.fam.name), f.trace.num_scenarios,
                                   f.trace.num_arrivals // max(f.trace.num_scenarios, 1)) for f in fams]
     wss = [torch.empty(orj.replay_seg_workspace_bytes(f.trace, g), dtype=torch.uint8, device=dev)
@@ -51,7 +51,7 @@ def main():
             rank_of = {i: k for k, i in enumerate(order)}
             streams = [torch.cuda.Stream(dev, priority=min(lo, hi + rank_of[i])) for i in range(len(fams))]
             i = order[-1]
-            segs[i] = bench.last_segments(spec, segs[i])   # as the bench: the family launched last
+            segs[i] = bench.last_segments(spec, segs[i], fams[i].trace.num_scenarios)  # as the bench
             wss[i] = torch.empty(orj.replay_seg_workspace_bytes(fams[i].trace, segs[i]), dtype=torch.uint8,
                                  device=dev)
             continue
