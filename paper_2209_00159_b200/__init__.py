@@ -193,6 +193,7 @@ class Queues:
     dist: torch.Tensor       # int32 [N]
     now: torch.Tensor        # int64 [Q]
     arrival: Optional[torch.Tensor] = None  # int64 [N], validation only
+    span: Optional[int] = None  # offsets[Q] - offsets[0] (host; read from the device once when not given)
 
     def __post_init__(self):
         _dev(self.offsets, torch.int64, "offsets")
@@ -208,11 +209,20 @@ class Queues:
     def num_queues(self):
         return self.now.numel()
 
+    @property
+    def members(self) -> int:
+        """Members covered by the offsets, offsets[Q] - offsets[0]: the row length
+        of the [S][N] priority outputs (the offsets may start at any base)."""
+        if self.span is None:
+            self.span = int(self.offsets[-1].item() - self.offsets[0].item())
+        return self.span
+
     @classmethod
     def from_numpy(cls, offsets, deadline, dist, now, arrival=None, device="cuda") -> "Queues":
         t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)  # noqa: E731
-        return cls(t(offsets, np.int64), t(deadline, np.int64), t(dist, np.int32), t(now, np.int64),
-                   None if arrival is None else t(arrival, np.int64))
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        return cls(t(off, np.int64), t(deadline, np.int64), t(dist, np.int32), t(now, np.int64),
+                   None if arrival is None else t(arrival, np.int64), int(off[-1] - off[0]))
 
     def validate(self, store: HistogramStore, stream=None):
         _abi.check(_abi.lib().orloj_validate_queues(store.c(), ctypes.byref(self._c), _stream_ptr(stream)))
@@ -278,9 +288,11 @@ class PriorityTable:
     def scores(self, queues: Queues, out: Optional[torch.Tensor] = None, stream=None, steps=None) -> torch.Tensor:
         """log p [S][N].  steps = (offset_ticks, cumulative_costs): piecewise-step
         cost, deadlines D_r + offset with cost c_s after each."""
-        N = queues.deadline.numel()
+        N = queues.members  # row length: offsets[Q] - offsets[0] (the kernel's [S][N] layout)
         if out is None:
             out = torch.empty((self.S, N), dtype=torch.float32, device=queues.now.device)
+        elif out.numel() < self.S * N:
+            raise OrlojError(1, f"out must hold num_sizes x {N} floats")
         if steps is None:
             _abi.check(_abi.lib().orloj_priority_scores(self.store.c(), self.profile.c(), self.S, self.b,
                                                         self.log_table.data_ptr(), self.log_expected.data_ptr(),
