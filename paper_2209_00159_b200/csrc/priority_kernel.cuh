@@ -562,28 +562,36 @@ __device__ __forceinline__ uint64_t pop_bitonic32(uint64_t me, int lane) {
 // the queue end hold 0.
 constexpr uint32_t POP_KNEG = 0x007fffffu;
 
+// order-preserving key of a log-priority: NaN -> fkey(-inf) (never selected),
+// -0 + 0 = +0 (-0 ties +0)
+__device__ __forceinline__ uint32_t pop_fkey(float x) {
+  const uint32_t u = __float_as_uint(fmaxf(x + 0.0f, -INFINITY));
+  return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
+
 // One queue of PopBatch: v[s] = log-priority of member 32 s + lane (any value
 // past the queue end, masked by n), bs in 1..S; lst: this warp's shared lists.
 __device__ __forceinline__ void pop_one(const float (&v)[8], int n, int bs, int lane, uint2 (*lst)[32],
                                         int32_t *__restrict__ out) {
-  uint32_t k[8];
+  // lane head (first maximal slot) and the best other value, on the raw
+  // floats: a NaN never wins a strict compare and fmaxf drops it; slot 0 is
+  // sanitised (NaN -> -inf), -0 == +0 compares equal (the first one is the
+  // head), slots past the queue end are -inf.  Only the head and the best other
+  // value are turned into keys (the general path below builds all 8).
+  const bool full = n >= 256;  // warp-uniform
+  float w[8];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    // NaN -> -inf (never selected), -0 + 0 = +0 (-0 ties +0)
-    const uint32_t u = __float_as_uint(fmaxf(v[s] + 0.0f, -INFINITY));
-    const uint32_t key = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);  // fkey
-    k[s] = (n >= 256 || 32 * s + lane < n) ? key : 0u;
-  }
-  // lane head (first maximal slot) and the best other key
-  uint32_t kh = k[0], k2 = 0u;
+  for (int s = 0; s < 8; ++s) w[s] = (full || 32 * s + lane < n) ? v[s] : -INFINITY;
+  float vh = fmaxf(w[0], -INFINITY), v2 = -INFINITY;
   int sh = 0;
 #pragma unroll
   for (int s = 1; s < 8; ++s) {
-    const bool gt = k[s] > kh;
-    k2 = gt ? kh : max(k2, k[s]);
+    const bool gt = w[s] > vh;
+    v2 = gt ? vh : fmaxf(v2, w[s]);
     sh = gt ? s : sh;
-    kh = gt ? k[s] : kh;
+    vh = gt ? w[s] : vh;
   }
+  const uint32_t kh = pop_fkey(vh), k2 = pop_fkey(v2);
   // worst selectable head (all-ones if none) and best non-head
   const uint32_t hsel = __reduce_min_sync(FULL, kh > POP_KNEG ? kh : 0xffffffffu);
   const uint32_t mx2 = __reduce_max_sync(FULL, k2);
@@ -609,9 +617,13 @@ __device__ __forceinline__ void pop_one(const float (&v)[8], int n, int bs, int 
     out[lane] = (lane < bs && (uint32_t)(me >> 32) > POP_KNEG) ? (int)~(uint32_t)me : -1;
     return;
   }
+  uint32_t k[8];
   int id[8];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) id[s] = 32 * s + lane;
+  for (int s = 0; s < 8; ++s) {
+    k[s] = (full || 32 * s + lane < n) ? pop_fkey(v[s]) : 0u;
+    id[s] = 32 * s + lane;
+  }
   // Batcher odd-even merge sort network for 8 (19 comparators), descending.
   cx(k[0], id[0], k[1], id[1]); cx(k[2], id[2], k[3], id[3]); cx(k[4], id[4], k[5], id[5]); cx(k[6], id[6], k[7], id[7]);
   cx(k[0], id[0], k[2], id[2]); cx(k[1], id[1], k[3], id[3]); cx(k[4], id[4], k[6], id[6]); cx(k[5], id[5], k[7], id[7]);
