@@ -579,17 +579,25 @@ __device__ __forceinline__ void pop_one(const float (&v)[8], int n, int bs, int 
   // head), slots past the queue end are -inf.  Only the head and the best other
   // value are turned into keys (the general path below builds all 8).
   const bool full = n >= 256;  // warp-uniform
-  float w[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) w[s] = (full || 32 * s + lane < n) ? v[s] : -INFINITY;
-  float vh = fmaxf(w[0], -INFINITY), v2 = -INFINITY;
+  float vh, v2 = -INFINITY;
   int sh = 0;
+  auto scan = [&](const float(&w)[8]) {
+    vh = fmaxf(w[0], -INFINITY);
 #pragma unroll
-  for (int s = 1; s < 8; ++s) {
-    const bool gt = w[s] > vh;
-    v2 = gt ? vh : fmaxf(v2, w[s]);
-    sh = gt ? s : sh;
-    vh = gt ? w[s] : vh;
+    for (int s = 1; s < 8; ++s) {
+      const bool gt = w[s] > vh;
+      v2 = gt ? vh : fmaxf(v2, w[s]);
+      sh = gt ? s : sh;
+      vh = gt ? w[s] : vh;
+    }
+  };
+  if (full) {
+    scan(v);
+  } else {
+    float w[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) w[s] = 32 * s + lane < n ? v[s] : -INFINITY;
+    scan(w);
   }
   const uint32_t kh = pop_fkey(vh), k2 = pop_fkey(v2);
   // worst selectable head (all-ones if none) and best non-head
