@@ -220,11 +220,14 @@ def _random_queues(seed, Q, D, B, kmax, maxlen):
 
 
 @pytest.mark.parametrize("B,kmax,maxlen", [(4, 1, 3), (12, 5, 9), (32, 32, 40), (36, 33, 70), (64, 100, 130),
-                                           (100, 64, 64), (132, 200, 260), (256, 256, 300), (252, 96, 120)])
+                                           (100, 64, 64), (132, 200, 260), (256, 256, 300), (252, 96, 120),
+                                           (20, 32, 45), (40, 32, 50), (52, 17, 30), (64, 32, 31)])
 def test_ragged_edges(B, kmax, maxlen):
     """Empty and ragged queues, n < kmax and n > kmax, B % 8 == 4 (half row
     vectors), every bins-per-lane / slot variant, sigma on exact bin edges and
-    +-1 tick, negative and huge slack, absolute times near 2^61."""
+    +-1 tick, negative and huge slack, absolute times near 2^61.  The last four
+    shapes (kmax <= 32, B <= 64) run the short-queue pick with one and two bins
+    per lane and B below a whole number of lanes."""
     counts, prof, q = _random_queues(B * 1000 + kmax, Q=67, D=9, B=B, kmax=kmax, maxlen=maxlen)
     _check_all(counts, prof, q, _run_all(counts, 1, prof, q))
 
