@@ -223,6 +223,17 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_edge_kernel(const __gr
   float *s_store = reinterpret_cast<float *>(s_row + 32);                           // [D][B] (smem_store)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   float *lgs = s_store + (p.smem_store ? (size_t)p.D * B : 0) + (size_t)wid * 32 * ROW;  // row k-1 = LG_k
+  // the queue's offsets / now are requested before the block stages its tables,
+  // so their latency overlaps the staging and the barriers
+  const int64_t q = (int64_t)blockIdx.x * MODEL_WARPS + wid;
+  const bool live = q < p.Q;
+  int64_t o0 = 0, o1 = 0, t = 0;
+  if (live) {
+    o0 = p.offsets[q];
+    o1 = p.offsets[q + 1];
+    t = p.now[q];
+  }
+  const int64_t base0 = p.offsets[0];
   if (p.smem_store)
     for (int e = threadIdx.x; e < p.D * B; e += blockDim.x) s_store[e] = p.log2F[e];
   lgs[lane * ROW] = -INFINITY;
@@ -237,16 +248,52 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_edge_kernel(const __gr
     for (int e = threadIdx.x; e < kmax * (B + 1); e += blockDim.x) s_dur[e] = p.dur[e];
   __syncthreads();
   const float *store = p.smem_store ? s_store : p.log2F;
-  const int64_t q = (int64_t)blockIdx.x * MODEL_WARPS + wid;
-  if (q >= p.Q) return;
-  const int64_t b0 = p.offsets[q] - p.offsets[0];
-  const int n = (int)(p.offsets[q + 1] - p.offsets[q]);
+  if (!live) return;
+  const int64_t b0 = o0 - base0;
+  const int n = (int)(o1 - o0);
   const int K = n < kmax ? n : kmax;
-  const int64_t t = p.now[q];
   const int64_t sig = lane < K ? p.deadline[b0 + lane] - t : 0;
   const int32_t s2 = sigma2(sig);  // ONE: the one unit step at offset 0
   const int dr = lane < K ? p.dist[b0 + lane] : 0;
 
+  float E = 0.f;
+  if (ONE && all_lin && p.smem_store) {
+    // one unit step, every row an arithmetic grid (Eq. 3), store in shared memory: the short-queue
+    // scorer's register-row form (score_small_kernel.cuh) — LG_k held across the
+    // lanes, member lane+1 looked up in it by one shuffle right after row k is
+    // added, no staged rows; the same adds, ex2 and butterfly as the staged form
+    // below, so the values are identical
+    float acc[BPL];
+#pragma unroll
+    for (int e = 0; e < BPL; ++e) acc[e] = 0.f;
+    int col[BPL];
+#pragma unroll
+    for (int e = 0; e < BPL; ++e) col[e] = min(32 * e + lane, B - 1);  // lanes past the last bin: never looked up
+    float pend[5];
+    const int nlane = -lane;
+    uint32_t ca[BPL];  // 32-bit shared-space address of the lane's column in row 0
+#pragma unroll
+    for (int e = 0; e < BPL; ++e) ca[e] = smem_base(s_store) + 4u * (uint32_t)col[e];
+    const uint32_t rb = smem_base(s_row);
+    const int dB4 = dr * B * 4;  // byte offset of member lane+1's row
+#pragma unroll
+    for (int k = 1; k <= 32; ++k) {
+      const uint32_t ro = (uint32_t)__shfl_sync(FULL, dB4, k - 1);  // rows past K: row 0, reach only E_k > K
+#pragma unroll
+      for (int e = 0; e < BPL; ++e) acc[e] += lds_f32_nv(ca[e] + ro);
+      const int4 rk = lds_v4s32(rb + 16u * (uint32_t)(k - 1));  // ModelRow {a2, wB2, mag, shl}
+      const int m = lookup_bin(s2, rk.x, rk.y, (uint32_t)rk.z, (uint32_t)rk.w & 31u);  // 1-based bin, 0: none
+      const int from = m - 1;                         // shfl takes the lane mod 32
+      float lg = __shfl_sync(FULL, acc[0], from);
+#pragma unroll
+      for (int e = 1; e < BPL; ++e) {
+        const float o = __shfl_sync(FULL, acc[e], from);
+        lg = (from >> 5) == e ? o : lg;
+      }
+      const float x = ex2_approx(lg);
+      E = bfly_push(pend, min(nlane + (k - 1), from) >= 0 ? x : 0.f, k - 1, lane);  // r <= k and m > 0
+    }
+  } else {
   // LG_k for k = 1..K (the same fp32 adds in the same order as the main scorer)
   float acc[BPL];
 #pragma unroll
@@ -265,7 +312,6 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_edge_kernel(const __gr
   __syncwarp();
 
   const uint32_t row0 = opaque_u32(smem_addr(lgs));
-  float E = 0.f;
   if (all_lin) {
     // every row an arithmetic grid: per cost step the main scorer's loop, no
     // branch per size (rows k > K are stale; they reach only E_k, k > K,
@@ -309,6 +355,7 @@ __global__ void __launch_bounds__(MODEL_WARPS * 32) model_edge_kernel(const __gr
     E = bfly_push(pend, v, k - 1, lane);
   }
   }
+  }  // staged rows
   const int k = lane + 1;
   const bool valid = k <= K;
   for (int kk = K + 1 + lane; kk <= kmax; kk += 32) p.E[q * kmax + kk - 1] = 0.f;
