@@ -52,23 +52,27 @@ cudaError_t launch_score_r(const ScoreParams &p, RowSrc src, cudaStream_t s) {
   return launch_score_s<BPL, PICK, false, false>(p, s);
 }
 
-// short queues over a small store: lanes over candidate sizes (score_small_kernel.cuh)
-template <int BPL, bool PICK>
+// short queues: lanes over candidate sizes (score_small_kernel.cuh), the store
+// staged in shared memory when small, else read from global memory per row
+template <int BPL, bool PICK, bool GSTORE>
 cudaError_t launch_score_small(const ScoreParams &p, cudaStream_t s) {
   const int64_t blocks = (p.Q + SMALL_WARPS - 1) / SMALL_WARPS;
-  const size_t smem = SmallShape<BPL>::bytes(p.D, p.B);
+  const size_t smem = GSTORE ? 0 : SmallShape<BPL>::bytes(p.D, p.B);
   static std::atomic<uint64_t> configured{0};
-  const size_t cap = (size_t)SMEM_STORE_BYTES;
-  cudaError_t e = ensure_max_dyn_smem(score_small_kernel<BPL, PICK>, (int)cap, configured);
+  const size_t cap = GSTORE ? 0 : (size_t)SMEM_STORE_BYTES;
+  cudaError_t e = ensure_max_dyn_smem(score_small_kernel<BPL, PICK, GSTORE>, (int)cap, configured);
   if (e != cudaSuccess) return e;
-  score_small_kernel<BPL, PICK><<<(unsigned)blocks, SMALL_WARPS * 32, smem, s>>>(p);
+  score_small_kernel<BPL, PICK, GSTORE><<<(unsigned)blocks, SMALL_WARPS * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 template <bool PICK>
 inline cudaError_t launch_score_b(const ScoreParams &p, RowSrc src, cudaStream_t s) {
-  if (src == RowSrc::Smem && p.kmax <= 32 && p.B <= 64 && !p.P && !p.EL)
-    return p.B <= 32 ? launch_score_small<1, PICK>(p, s) : launch_score_small<2, PICK>(p, s);
+  if (p.kmax <= 32 && p.B <= 64 && !p.P && !p.EL) {
+    if (src == RowSrc::Smem)
+      return p.B <= 32 ? launch_score_small<1, PICK, false>(p, s) : launch_score_small<2, PICK, false>(p, s);
+    return p.B <= 32 ? launch_score_small<1, PICK, true>(p, s) : launch_score_small<2, PICK, true>(p, s);
+  }
   switch (bins_per_lane(p.B)) {
     case 1: return launch_score_r<1, PICK>(p, src, s);
     case 2: return launch_score_r<2, PICK>(p, src, s);

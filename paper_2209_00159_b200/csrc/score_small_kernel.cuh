@@ -33,7 +33,9 @@ struct SmallShape {
   __host__ __device__ static size_t bytes(int D, int B) { return ((size_t)D * B * 4 + 15) & ~(size_t)15; }
 };
 
-template <int BPL, bool PICK>
+// GSTORE: the store stays in global memory (too large to stage: e.g. one row
+// per request), each lane reading its bins of member k's row (read-only path)
+template <int BPL, bool PICK, bool GSTORE = false>
 __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __grid_constant__ ScoreParams p) {
   extern __shared__ __align__(16) float s_dyn[];
   const int lane = threadIdx.x & 31;
@@ -53,9 +55,11 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
   }
   const int64_t base0 = p.offsets[0];  // offsets may start at any base (chunked calls)
 
-  for (int e = threadIdx.x * 4; e < D * B; e += blockDim.x * 4)
-    *reinterpret_cast<float4 *>(s_store + e) = __ldg(reinterpret_cast<const float4 *>(p.log2F + e));
-  __syncthreads();
+  if constexpr (!GSTORE) {
+    for (int e = threadIdx.x * 4; e < D * B; e += blockDim.x * 4)
+      *reinterpret_cast<float4 *>(s_store + e) = __ldg(reinterpret_cast<const float4 *>(p.log2F + e));
+    __syncthreads();
+  }
 
   if (!live) return;
   const int64_t off = o0 - base0;
@@ -70,7 +74,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
     dd = p.dist[j];
   }
   const int32_t sig = lane < K ? sigma2(dl - now) : 0;  // lanes >= K: bin 0, P = 0
-  const int idB = lane < K ? dd * B * 4 : 0;            // byte offset of member lane's row
+  const int idB = lane < K ? dd * B * 4 : 0;            // byte offset of member lane's row (shared store)
+  const int idR = lane < K ? dd : 0;                    // member lane's row (global store)
   // a lane's store column per vector (lanes past the last bin re-read bin B - 1:
   // in bounds, never looked up since i* <= B)
   uint32_t col[BPL];
@@ -86,9 +91,15 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32) score_small_kernel(const __g
 #pragma unroll
   for (int k = 1; k <= 32; ++k) {
     // a2: LG_k over the lanes (rows past K add row 0: they only reach E_k for k > K)
-    const uint32_t rk = (uint32_t)__shfl_sync(FULL, idB, k - 1);
+    if constexpr (GSTORE) {
+      const float *row = p.log2F + (int64_t)__shfl_sync(FULL, idR, k - 1) * B;
 #pragma unroll
-    for (int e = 0; e < BPL; ++e) acc[e] += lds_f32_nv(col[e] + rk);  // read-only store: free to issue ahead
+      for (int e = 0; e < BPL; ++e) acc[e] += __ldg(row + min(lane + 32 * e, B - 1));
+    } else {
+      const uint32_t rk = (uint32_t)__shfl_sync(FULL, idB, k - 1);
+#pragma unroll
+      for (int e = 0; e < BPL; ++e) acc[e] += lds_f32_nv(col[e] + rk);  // read-only store: free to issue ahead
+    }
     // a3-a4: member lane+1 at size k (constants beyond kmax are 0: bin 0)
     const int bi = lookup_bin(sig, p.prof.a2[k - 1], p.prof.wB2[k - 1], p.prof.mag[k - 1], p.prof.sh[k - 1]);
     const int from = bi - 1;  // shfl takes the source lane mod 32 (bi = 0: masked below)

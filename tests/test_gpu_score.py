@@ -342,10 +342,13 @@ def test_store_build_values():
     assert np.abs(np.exp2(L[nz]) - F[nz]).max() <= 1e-6
 
 
-@pytest.mark.parametrize("B,kmax,maxlen", [(16, 8, 12), (64, 40, 70), (100, 64, 64), (132, 130, 140)])
+@pytest.mark.parametrize("B,kmax,maxlen", [(16, 8, 12), (64, 40, 70), (100, 64, 64), (132, 130, 140),
+                                           (40, 20, 30), (64, 32, 45)])
 def test_tma_row_path(B, kmax, maxlen):
     """Per-request rows (store > 48 KiB, so rows come through the TMA ring
-    rather than the shared-memory store) for every bins-per-lane variant."""
+    rather than the shared-memory store) for every bins-per-lane variant; with
+    kmax <= 32 and B <= 64 the pick and E-only score take the short-queue
+    kernel reading its rows from global memory (one and two bins per lane)."""
     counts, prof, q = _random_queues(7 * B + kmax, Q=97, D=9, B=B, kmax=kmax, maxlen=maxlen)
     rng = np.random.default_rng(B)
     D = max(9, (64 << 10) // (4 * B) + 1)
