@@ -25,7 +25,10 @@
 
 namespace orloj {
 
-constexpr int SMALL_WARPS = 8;
+#ifndef ORLOJ_SMALL_WARPS
+#define ORLOJ_SMALL_WARPS 4
+#endif
+constexpr int SMALL_WARPS = ORLOJ_SMALL_WARPS;  // queues (warps) per block
 
 // shared memory: the store [D][B]
 template <int BPL>
