@@ -1252,7 +1252,6 @@ def shard_proxy(args, dev, ms_full):
                          "ms_min_over_ranks": min(per_rank), "imbalance": mx / min(per_rank),
                          "implied_speedup": ms_full / mx, "segments_per_scenario": segs}
     return proxy
-    return out
 
 
 if __name__ == "__main__":
